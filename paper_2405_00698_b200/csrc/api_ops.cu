@@ -1,0 +1,166 @@
+// api_ops.cu — C ABI: genome sampling, decode, component, build, evaluate,
+// diversity (host- and device-pointer entry points).
+#include <vector>
+
+#include "vx_ga.cuh"
+#include "vx_internal.cuh"
+
+using namespace vx;
+
+namespace {
+
+template <typename T>
+vx_status upload(DevBuf<T>& buf, const T* h, size_t n, cudaStream_t s) {
+    VX_TRY(buf.alloc(n));
+    VX_CUDA(cudaMemcpyAsync(buf.p, h, n * sizeof(T), cudaMemcpyHostToDevice, s));
+    return VX_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+vx_status vx_sample_genomes_dev(vx_ctx* ctx, const vx_arch* a, int32_t P, const uint64_t* d_seeds, double* d_params,
+                                double* d_bmat) {
+    if (!ctx || !a || P < 0) return VX_EINVAL;
+    return sample_genomes_dev(ctx, a, P, d_seeds, d_params, d_bmat);
+}
+
+vx_status vx_decode_dev(vx_ctx* ctx, const vx_arch* a, int32_t P, const double* d_params, const double* d_bmat,
+                        int32_t w, int32_t h, int32_t d, uint8_t* d_mat, double* d_weight, uint32_t* d_guard) {
+    if (!ctx || !a || P < 0) return VX_EINVAL;
+    return decode_dev(ctx, a, P, d_params, d_bmat, w, h, d, d_mat, d_weight, d_guard, nullptr, 0);
+}
+
+vx_status vx_decode(vx_ctx* ctx, const vx_arch* a, int32_t P, const double* params, const double* bmat, int32_t w,
+                    int32_t h, int32_t d, uint8_t* mat, double* weight) {
+    if (!ctx || !a || P < 0 || !params || !bmat) return VX_EINVAL;
+    if (w < 1 || h < 1 || d < 1) return (set_error("decode: dims must be positive"), VX_EINVAL);
+    const int64_t np = param_count(a);
+    if (np < 0) return (set_error("invalid architecture"), VX_EINVAL);
+    const size_t cells = static_cast<size_t>(w) * h * d;
+    DevBuf<double> dp, db, dw;
+    DevBuf<uint8_t> dm;
+    VX_TRY(upload(dp, params, P * static_cast<size_t>(np), ctx->stream));
+    VX_TRY(upload(db, bmat, P * 3ull * a->m, ctx->stream));
+    VX_TRY(dm.alloc(P * cells));
+    VX_TRY(dw.alloc(P * cells));
+    VX_TRY(decode_dev(ctx, a, P, dp.p, db.p, w, h, d, dm.p, dw.p, nullptr, nullptr, 0));
+    VX_CUDA(cudaMemcpyAsync(mat, dm.p, P * cells, cudaMemcpyDeviceToHost, ctx->stream));
+    VX_CUDA(cudaMemcpyAsync(weight, dw.p, P * cells * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    VX_CUDA(cudaStreamSynchronize(ctx->stream));
+    return VX_OK;
+}
+
+vx_status vx_largest_component_dev(vx_ctx* ctx, int32_t P, int32_t w, int32_t h, int32_t d, const uint8_t* d_in,
+                                   uint8_t* d_out) {
+    if (!ctx || P < 0 || w < 1 || h < 1 || d < 1) return VX_EINVAL;
+    return largest_component_dev(ctx, P, w, h, d, d_in, d_out, nullptr);
+}
+
+vx_status vx_largest_component(vx_ctx* ctx, int32_t P, int32_t w, int32_t h, int32_t d, const uint8_t* in,
+                               uint8_t* out) {
+    if (!ctx || P < 0 || w < 1 || h < 1 || d < 1 || !in || !out) return VX_EINVAL;
+    const size_t cells = static_cast<size_t>(w) * h * d;
+    DevBuf<uint8_t> di, dout;
+    VX_TRY(upload(di, in, P * cells, ctx->stream));
+    VX_TRY(dout.alloc(P * cells));
+    VX_TRY(largest_component_dev(ctx, P, w, h, d, di.p, dout.p, nullptr));
+    VX_CUDA(cudaMemcpyAsync(out, dout.p, P * cells, cudaMemcpyDeviceToHost, ctx->stream));
+    VX_CUDA(cudaStreamSynchronize(ctx->stream));
+    return VX_OK;
+}
+
+vx_status vx_batch_build_dev(vx_ctx* ctx, int32_t P, int32_t w, int32_t h, int32_t d, const uint8_t* d_mat,
+                             const double* d_weight, const vx_materials* table, const vx_plane* plane,
+                             vx_batch** out) {
+    if (!ctx || !table || !plane || !out || P < 0) return VX_EINVAL;
+    auto* b = new vx_batch;
+    vx_status st = build_batch_into(ctx, b, P, w, h, d, d_mat, d_weight, nullptr, table, plane);
+    if (st != VX_OK) {
+        delete b;
+        return st;
+    }
+    *out = b;
+    return VX_OK;
+}
+
+vx_status vx_batch_build(vx_ctx* ctx, int32_t P, int32_t w, int32_t h, int32_t d, const uint8_t* mat,
+                         const double* weight, const vx_materials* table, const vx_plane* plane, vx_batch** out) {
+    if (!ctx || !mat || !weight || P < 0) return VX_EINVAL;
+    if (w < 1 || h < 1 || d < 1) return (set_error("dims must be positive"), VX_EINVAL);
+    const size_t cells = static_cast<size_t>(w) * h * d;
+    DevBuf<uint8_t> dm;
+    DevBuf<double> dw;
+    VX_TRY(upload(dm, mat, P * cells, ctx->stream));
+    VX_TRY(upload(dw, weight, P * cells, ctx->stream));
+    VX_TRY(vx_batch_build_dev(ctx, P, w, h, d, dm.p, dw.p, table, plane, out));
+    VX_CUDA(cudaStreamSynchronize(ctx->stream));
+    return VX_OK;
+}
+
+vx_status vx_evaluate_dev(vx_ctx* ctx, int32_t P, int32_t w, int32_t h, int32_t d, const uint8_t* d_mat,
+                          const double* d_weight, const vx_materials* table, const vx_plane* plane, const vx_sim* sim,
+                          const int32_t* d_todo, int32_t n_todo, double* d_fitness, vx_summary* d_summaries) {
+    if (!ctx || !table || !plane || !sim || P < 0) return VX_EINVAL;
+    if (w < 1 || h < 1 || d < 1) return (set_error("dims must be positive"), VX_EINVAL);
+    return evaluate_pipeline(ctx, P, w, h, d, d_mat, d_weight, table, plane, sim, d_todo, n_todo, d_fitness, nullptr,
+                             d_summaries);
+}
+
+vx_status vx_evaluate(vx_ctx* ctx, int32_t P, int32_t w, int32_t h, int32_t d, const uint8_t* mat,
+                      const double* weight, const vx_materials* table, const vx_plane* plane, const vx_sim* sim,
+                      double* fitness, vx_summary* summaries) {
+    if (!ctx || !mat || !weight || !fitness || P < 0) return VX_EINVAL;
+    if (w < 1 || h < 1 || d < 1) return (set_error("dims must be positive"), VX_EINVAL);
+    const size_t cells = static_cast<size_t>(w) * h * d;
+    DevBuf<uint8_t> dm;
+    DevBuf<double> dw, df;
+    DevBuf<vx_summary> ds;
+    VX_TRY(upload(dm, mat, P * cells, ctx->stream));
+    VX_TRY(upload(dw, weight, P * cells, ctx->stream));
+    VX_TRY(df.alloc(P));
+    if (summaries) VX_TRY(ds.alloc(P));
+    VX_TRY(evaluate_pipeline(ctx, P, w, h, d, dm.p, dw.p, table, plane, sim, nullptr, P, df.p, nullptr,
+                             summaries ? ds.p : nullptr));
+    VX_CUDA(cudaMemcpyAsync(fitness, df.p, P * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    if (summaries)
+        VX_CUDA(cudaMemcpyAsync(summaries, ds.p, P * sizeof(vx_summary), cudaMemcpyDeviceToHost, ctx->stream));
+    VX_CUDA(cudaStreamSynchronize(ctx->stream));
+    return VX_OK;
+}
+
+vx_status vx_material_histogram_dev(vx_ctx* ctx, int32_t P, int32_t cells, const uint8_t* d_mat, int64_t* d_hist,
+                                    int32_t accumulate) {
+    if (!ctx || P < 0 || cells < 0) return VX_EINVAL;
+    return histogram_dev(ctx, P, cells, d_mat, d_hist, accumulate != 0);
+}
+
+vx_status vx_diversity_from_histogram_dev(vx_ctx* ctx, int32_t P, int32_t cells, const int64_t* d_hist,
+                                          double* d_out) {
+    if (!ctx || P < 0 || cells < 0) return VX_EINVAL;
+    return diversity_from_hist_dev(ctx, P, cells, d_hist, d_out);
+}
+
+vx_status vx_population_diversity_dev(vx_ctx* ctx, int32_t P, int32_t cells, const uint8_t* d_mat, double* d_out) {
+    if (!ctx || P < 0 || cells < 0) return VX_EINVAL;
+    DevBuf<int64_t> hist;
+    VX_TRY(hist.alloc(static_cast<size_t>(cells) * VX_NMAT + 1));
+    VX_TRY(histogram_dev(ctx, P, cells, d_mat, hist.p, false));
+    VX_TRY(diversity_from_hist_dev(ctx, P, cells, hist.p, d_out));
+    VX_CUDA(cudaStreamSynchronize(ctx->stream));  // hist is freed on return
+    return VX_OK;
+}
+
+vx_status vx_population_diversity(vx_ctx* ctx, int32_t P, int32_t cells, const uint8_t* mat, double* out) {
+    if (!ctx || P < 0 || cells < 0 || !out) return VX_EINVAL;
+    DevBuf<uint8_t> dm;
+    DevBuf<double> dd;
+    VX_TRY(upload(dm, mat, static_cast<size_t>(P) * cells, ctx->stream));
+    VX_TRY(dd.alloc(1));
+    VX_TRY(vx_population_diversity_dev(ctx, P, cells, dm.p, dd.p));
+    VX_CUDA(cudaMemcpy(out, dd.p, sizeof(double), cudaMemcpyDeviceToHost));
+    return VX_OK;
+}
+
+}  // extern "C"

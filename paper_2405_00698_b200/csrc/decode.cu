@@ -1,0 +1,380 @@
+// decode.cu — K1-K3 (decode) and K14 (genome sampling) on device.
+//
+// K1-K3 replace decode (morphology.hpp:141-157) over forward
+// (genome.hpp:187-211), gaussian_encode (:169-179), affine (:118-126) and
+// stable_sigmoid (:128-138) for a whole population:
+//  * one CTA per genome keeps the genome's parameters resident in shared
+//    memory (8710 FP64 = 68 KB for the default architecture) and sweeps the
+//    robot's voxels in tiles of 32 (one voxel per lane);
+//  * every affine keeps the reference's sequential order acc = b; acc +=
+//    w*x (c ascending) with separately rounded mul/add (compiled --fmad=false),
+//    so pre-activations are bit-identical given identical inputs; the
+//    activations are stored [feature][voxel] so W rows are warp broadcasts and
+//    activations are conflict-free;
+//  * epilogue: softmax (first max, ordered sum), strict-> argmax (ties to the
+//    lowest material), stable sigmoid + both clamps, and a guard counter for
+//    voxels whose top-2 probability gap is < 1e-12 (where device vs glibc
+//    transcendentals could flip the argmax — never observed).
+// FP64 is the reference's precision; tcgen05 has no f64 kind and B200 runs
+// DMMA at the FP64 vector rate, so the CUDA-core form with exact ordering is
+// used (decode is < 1% of a generation).
+//
+// K14 replaces sample_genome (genome.hpp:146-166): one warp per genome runs
+// its own mt19937_64 (warp-parallel twist, smem state), W entries are exact
+// uniform draws; B uses device log/cos (ulp-level vs glibc).
+#include <cmath>
+
+#include "vx_internal.cuh"
+
+namespace vx {
+
+int64_t param_count(const vx_arch* a) {
+    if (!a || a->m < 1 || a->n_hidden < 0 || a->n_hidden > VX_MAX_HIDDEN) return -1;
+    int64_t n = 0;
+    int64_t in = 2LL * a->m;
+    for (int l = 0; l < a->n_hidden; ++l) {
+        if (a->hidden[l] < 1) return -1;
+        n += in * a->hidden[l] + a->hidden[l];
+        in = a->hidden[l];
+    }
+    n += in * VX_NMAT + VX_NMAT;
+    n += in + 1;
+    return n;
+}
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+constexpr int kTile = 32;
+
+struct DecodeArgs {
+    int m, nh;
+    int widths[VX_MAX_HIDDEN];
+    int64_t np;
+    int max_width;  // max(2m, hidden...)
+    int w, h, d;
+    const double* params;
+    const double* bmat;
+    const int32_t* select;
+    uint8_t* mat;
+    double* weight;
+    uint32_t* guard;
+    bool params_in_smem;
+};
+
+__device__ __forceinline__ double stable_sigmoid(double z) {
+    double s;
+    if (z >= 0.0) {
+        s = 1.0 / (1.0 + exp(-z));
+    } else {
+        const double e = exp(z);
+        s = e / (1.0 + e);
+    }
+    if (s < 1e-12) s = 1e-12;
+    if (s > 1.0 - 1e-12) s = 1.0 - 1e-12;
+    return s;
+}
+
+__global__ void __launch_bounds__(kThreads) decode_kernel(DecodeArgs A) {
+    const int g = A.select ? A.select[blockIdx.x] : static_cast<int>(blockIdx.x);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    double* sm = reinterpret_cast<double*>(smem_raw);
+    const double* gp = A.params + static_cast<size_t>(g) * A.np;
+    const double* P;
+    if (A.params_in_smem) {
+        double* sp = sm;
+        for (int64_t q = threadIdx.x; q < A.np; q += kThreads) sp[q] = gp[q];
+        P = sp;
+        sm += A.np;
+    } else {
+        P = gp;
+    }
+    double* Bm = sm;  // 3m
+    sm += 3 * A.m;
+    double* X = sm;  // [feature][kTile]
+    double* Y = sm + static_cast<size_t>(A.max_width) * kTile;
+    double* L = Y + static_cast<size_t>(A.max_width) * kTile;  // logits [6][kTile]
+    for (int q = threadIdx.x; q < 3 * A.m; q += kThreads) Bm[q] = A.bmat[static_cast<size_t>(g) * 3 * A.m + q];
+    __syncthreads();
+
+    const int ncell = A.w * A.h * A.d;
+    const int m = A.m;
+    for (int t0 = 0; t0 < ncell; t0 += kTile) {
+        const int cell = t0 + lane;
+        const bool live = cell < ncell;
+        double v0 = 0.0, v1 = 0.0, v2 = 0.0;
+        if (live) {
+            const int x = cell % A.w, y = (cell / A.w) % A.h, z = cell / (A.w * A.h);
+            v0 = (x + 0.5) / A.w;  // morphology.hpp:147
+            v1 = (y + 0.5) / A.h;
+            v2 = (z + 0.5) / A.d;
+        }
+        // gaussian_encode (genome.hpp:169-179)
+        for (int r = wid; r < m; r += kWarps) {
+            const double phase = kTwoPi * (Bm[3 * r] * v0 + Bm[3 * r + 1] * v1 + Bm[3 * r + 2] * v2);
+            double sn, cs;
+            sincos(phase, &sn, &cs);
+            X[r * kTile + lane] = cs;
+            X[(m + r) * kTile + lane] = sn;
+        }
+        __syncthreads();
+        // hidden layers: affine (genome.hpp:118-126) + tanh (:192)
+        int in = 2 * m;
+        const double* lp = P;
+        for (int l = 0; l < A.nh; ++l) {
+            const int out = A.widths[l];
+            const double* W = lp;
+            const double* b = lp + static_cast<int64_t>(in) * out;
+            for (int r = wid; r < out; r += kWarps) {
+                const double* wr = W + static_cast<int64_t>(r) * in;
+                double acc = b[r];
+                for (int c = 0; c < in; ++c) acc += wr[c] * X[c * kTile + lane];
+                Y[r * kTile + lane] = tanh(acc);
+            }
+            __syncthreads();
+            double* t = X;
+            X = Y;
+            Y = t;
+            lp = b + out;
+            in = out;
+        }
+        // heads: 5 material logits then 1 weight logit
+        {
+            const double* Wm = lp;
+            const double* bm = lp + static_cast<int64_t>(in) * VX_NMAT;
+            const double* Ww = bm + VX_NMAT;
+            const double* bw = Ww + in;
+            for (int r = wid; r < VX_NMAT + 1; r += kWarps) {
+                const double* wr = r < VX_NMAT ? Wm + static_cast<int64_t>(r) * in : Ww;
+                double acc = r < VX_NMAT ? bm[r] : bw[0];
+                for (int c = 0; c < in; ++c) acc += wr[c] * X[c * kTile + lane];
+                L[r * kTile + lane] = acc;
+            }
+        }
+        __syncthreads();
+        if (wid == 0 && live) {
+            double lg[VX_NMAT];
+            for (int i = 0; i < VX_NMAT; ++i) lg[i] = L[i * kTile + lane];
+            double mx = lg[0];  // std::max_element: first maximal
+            for (int i = 1; i < VX_NMAT; ++i)
+                if (mx < lg[i]) mx = lg[i];
+            double p[VX_NMAT];
+            double sum = 0.0;
+            for (int i = 0; i < VX_NMAT; ++i) {
+                p[i] = exp(lg[i] - mx);
+                sum += p[i];
+            }
+            for (int i = 0; i < VX_NMAT; ++i) p[i] /= sum;
+            int best = 0;
+            for (int i = 1; i < VX_NMAT; ++i)
+                if (p[i] > p[best]) best = i;
+            if (A.guard) {
+                double second = -1.0;
+                for (int i = 0; i < VX_NMAT; ++i)
+                    if (i != best && p[i] > second) second = p[i];
+                if (p[best] - second < 1e-12 * p[best]) atomicAdd(A.guard, 1u);
+            }
+            double wgt = stable_sigmoid(L[VX_NMAT * kTile + lane]);
+            wgt = wgt < kMinVoxelWeight ? kMinVoxelWeight : (wgt > 1.0 ? 1.0 : wgt);  // morphology.hpp:154
+            const size_t o = static_cast<size_t>(g) * ncell + cell;
+            A.mat[o] = static_cast<uint8_t>(best);
+            A.weight[o] = wgt;
+        }
+        __syncthreads();
+    }
+}
+
+// ------------------------------------------------------------ K14: mt19937_64
+constexpr int kMtN = 312, kMtM = 156;
+constexpr int kSampleWarps = 4;  // 4 x 7.3 KB of mt19937_64 state per CTA
+constexpr uint64_t kUM = 0xFFFFFFFF80000000ULL, kLM = 0x7FFFFFFFULL, kMatA = 0xB5026F5AA96619E9ULL;
+
+__device__ __forceinline__ uint64_t mt_mix(uint64_t cur, uint64_t nxt, uint64_t far) {
+    const uint64_t y = (cur & kUM) | (nxt & kLM);
+    return far ^ (y >> 1) ^ ((y & 1ULL) ? kMatA : 0ULL);
+}
+
+__device__ __forceinline__ uint64_t mt_temper(uint64_t z) {
+    z ^= (z >> 29) & 0x5555555555555555ULL;
+    z ^= (z << 17) & 0x71D67FFFEDA60000ULL;
+    z ^= (z << 37) & 0xFFF7EEE000000000ULL;
+    z ^= z >> 43;
+    return z;
+}
+
+// Warp-parallel twist: old state in A, new state written to B (2 phases + tail).
+__device__ void warp_twist(const uint64_t* A, uint64_t* B, int lane) {
+    for (int i = lane; i < kMtN - kMtM; i += 32) B[i] = mt_mix(A[i], A[i + 1], A[i + kMtM]);
+    __syncwarp();
+    for (int i = kMtN - kMtM + lane; i < kMtN - 1; i += 32) B[i] = mt_mix(A[i], A[i + 1], B[i - (kMtN - kMtM)]);
+    __syncwarp();
+    if (lane == 0) B[kMtN - 1] = mt_mix(A[kMtN - 1], B[0], B[kMtM - 1]);
+    __syncwarp();
+}
+
+struct SampleArgs {
+    int m, nh;
+    int widths[VX_MAX_HIDDEN];
+    int64_t np;
+    double sigma;
+    int P;
+    const uint64_t* seeds;
+    double* params;
+    double* bmat;
+};
+
+// One warp per genome.  Draw t of the genome stream is tempered word t % 312
+// of twist t / 312 (the first twist happens before draw 0).
+__global__ void __launch_bounds__(kSampleWarps * 32) sample_kernel(SampleArgs A) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int g = blockIdx.x * kSampleWarps + wid;
+    __shared__ uint64_t s_state[kSampleWarps][2][kMtN];
+    __shared__ uint64_t s_out[kSampleWarps][kMtN];
+    if (g >= A.P) return;
+    uint64_t* S0 = s_state[wid][0];
+    uint64_t* S1 = s_state[wid][1];
+    uint64_t* O = s_out[wid];
+    double* params = A.params + static_cast<size_t>(g) * A.np;
+    double* bmat = A.bmat + static_cast<size_t>(g) * 3 * A.m;
+    // seeding (sequential recurrence, lane 0)
+    if (lane == 0) {
+        uint64_t x = A.seeds[g];
+        S0[0] = x;
+        for (int i = 1; i < kMtN; ++i) {
+            x = 6364136223846793005ULL * (x ^ (x >> 62)) + static_cast<uint64_t>(i);
+            S0[i] = x;
+        }
+    }
+    __syncwarp();
+    // zero biases; W filled from the stream below
+    {
+        int64_t off = 0;
+        int in = 2 * A.m;
+        for (int l = 0; l <= A.nh + 1; ++l) {
+            const int out = l < A.nh ? A.widths[l] : (l == A.nh ? VX_NMAT : 1);
+            off += static_cast<int64_t>(in) * out;
+            for (int q = lane; q < out; q += 32) params[off + q] = 0.0;
+            off += out;
+            if (l < A.nh) in = out;
+        }
+    }
+    const int64_t n_b_draws = 6LL * A.m;  // 3m normals, 2 draws each
+    int64_t n_w = 0;
+    {
+        int in = 2 * A.m;
+        for (int l = 0; l < A.nh; ++l) {
+            n_w += static_cast<int64_t>(in) * A.widths[l];
+            in = A.widths[l];
+        }
+        n_w += static_cast<int64_t>(in) * VX_NMAT + in;
+    }
+    const int64_t total = n_b_draws + n_w;
+    uint64_t* cur = S0;
+    uint64_t* nxt = S1;
+    for (int64_t base = 0; base < total; base += kMtN) {
+        warp_twist(cur, nxt, lane);
+        uint64_t* t = cur;
+        cur = nxt;
+        nxt = t;
+        for (int i = lane; i < kMtN; i += 32) O[i] = mt_temper(cur[i]);
+        __syncwarp();
+        for (int i = lane; i < kMtN; i += 32) {
+            const int64_t dix = base + i;
+            if (dix >= total) break;
+            if (dix < n_b_draws) {
+                if ((dix & 1) == 0) {  // Rng::normal (rng.hpp:26-30) on draws dix, dix+1
+                    const double u1 = (static_cast<double>(O[i] >> 11) + 0.5) * 0x1.0p-53;
+                    const double u2 = static_cast<double>(O[i + 1] >> 11) * 0x1.0p-53;
+                    const double nrm = sqrt(-2.0 * log(u1)) * cos(2.0 * M_PI * u2);
+                    bmat[dix >> 1] = A.sigma * nrm;
+                }
+            } else {
+                // uniform W entry: locate its tensor (init_layer, genome.hpp:106-115)
+                int64_t q = dix - n_b_draws;
+                int64_t off = 0;
+                int in = 2 * A.m;
+                for (int l = 0; l <= A.nh + 1; ++l) {
+                    const int out = l < A.nh ? A.widths[l] : (l == A.nh ? VX_NMAT : 1);
+                    const int64_t nw = static_cast<int64_t>(in) * out;
+                    if (q < nw) {
+                        const double limit = sqrt(6.0 / static_cast<double>(in + out));
+                        const double u = static_cast<double>(O[i] >> 11) * 0x1.0p-53;
+                        params[off + q] = (2.0 * u - 1.0) * limit;
+                        break;
+                    }
+                    q -= nw;
+                    off += nw + out;
+                    if (l < A.nh) in = out;
+                }
+            }
+        }
+        __syncwarp();
+    }
+}
+
+}  // namespace
+
+vx_status decode_dev(vx_ctx* ctx, const vx_arch* a, int P, const double* d_params, const double* d_bmat, int w, int h,
+                     int d, uint8_t* d_mat, double* d_weight, uint32_t* d_guard, const int32_t* d_select,
+                     int n_select) {
+    const int64_t np = param_count(a);
+    if (np < 0) return (set_error("invalid architecture"), VX_EINVAL);
+    if (w < 1 || h < 1 || d < 1) return (set_error("decode: dims must be positive"), VX_EINVAL);
+    const int n = d_select ? n_select : P;
+    if (n <= 0) return VX_OK;
+    DecodeArgs A{};
+    A.m = a->m;
+    A.nh = a->n_hidden;
+    int maxw = 2 * a->m;
+    for (int l = 0; l < a->n_hidden; ++l) {
+        A.widths[l] = a->hidden[l];
+        maxw = maxw > a->hidden[l] ? maxw : a->hidden[l];
+    }
+    A.np = np;
+    A.max_width = maxw;
+    A.w = w;
+    A.h = h;
+    A.d = d;
+    A.params = d_params;
+    A.bmat = d_bmat;
+    A.select = d_select;
+    A.mat = d_mat;
+    A.weight = d_weight;
+    A.guard = d_guard;
+    const size_t act = (2ull * maxw + VX_NMAT + 1) * kTile * sizeof(double) + 3ull * a->m * sizeof(double);
+    size_t smem = act + static_cast<size_t>(np) * sizeof(double);
+    A.params_in_smem = smem + 1024 <= ctx->smem_optin;
+    if (!A.params_in_smem) smem = act;
+    if (smem > ctx->smem_optin) return (set_error("decode: architecture too wide"), VX_EINVAL);
+    VX_CUDA(cudaFuncSetAttribute(decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    decode_kernel<<<n, kThreads, smem, ctx->stream>>>(A);
+    ctx->launches++;
+    VX_CUDA(cudaGetLastError());
+    return VX_OK;
+}
+
+vx_status sample_genomes_dev(vx_ctx* ctx, const vx_arch* a, int P, const uint64_t* d_seeds, double* d_params,
+                             double* d_bmat) {
+    const int64_t np = param_count(a);
+    if (np < 0) return (set_error("invalid architecture"), VX_EINVAL);
+    if (!(a->sigma > 0.0)) return (set_error("EncodingSpec: sigma must be > 0"), VX_EINVAL);
+    if (P <= 0) return VX_OK;
+    SampleArgs A{};
+    A.m = a->m;
+    A.nh = a->n_hidden;
+    for (int l = 0; l < a->n_hidden; ++l) A.widths[l] = a->hidden[l];
+    A.np = np;
+    A.sigma = a->sigma;
+    A.P = P;
+    A.seeds = d_seeds;
+    A.params = d_params;
+    A.bmat = d_bmat;
+    sample_kernel<<<ceil_div(P, kSampleWarps), kSampleWarps * 32, 0, ctx->stream>>>(A);
+    ctx->launches++;
+    VX_CUDA(cudaGetLastError());
+    return VX_OK;
+}
+
+}  // namespace vx

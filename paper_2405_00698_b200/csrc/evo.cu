@@ -1,0 +1,535 @@
+// evo.cu — device-resident EvolutionState and evolve_generation
+// (evolution.hpp:177-293), plus the fused evaluate pipeline.
+//
+// Per generation:
+//   begin : decode the individuals without a cached grid (replicated on every
+//           rank), evaluate this rank's shard of the not-yet-evaluated ones
+//           (component -> build -> gates -> fused integrator), and START the
+//           breeding-plan parse on a host thread: the mt19937_64 draw sequence
+//           of a generation depends only on (RNG state, HyperParams, P), never
+//           on fitness, so the sequential stream parse
+//           overlaps the GPU simulation;
+//   [caller all-reduces the exchange buffer when world > 1]
+//   finish: merge fitness, stable sort (CUB), sequential stats, histogram
+//           diversity, best genome, then apply the plan on device (elite copy,
+//           tournament parents gathered by sorted rank, crossover masks,
+//           mutation deltas) into the double-buffered population.
+// All RNG consumption and every GA decision are bit-identical to the
+// reference; mutation noise uses the host glibc normal() exactly as the
+// reference does.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <random>
+#include <sstream>
+#include <thread>
+#include <vector>
+
+#include "vx_ga.cuh"
+#include "vx_internal.cuh"
+
+using namespace vx;
+
+namespace vx {
+
+// raw grids -> component -> build -> gates -> integrate -> fitness
+vx_status evaluate_pipeline(vx_ctx* ctx, int P, int w, int h, int d, const uint8_t* d_mat, const double* d_weight,
+                            const vx_materials* table, const vx_plane* plane, const vx_sim* sim, const int32_t* d_todo,
+                            int n_todo, double* d_fitness, double* d_updates, vx_summary* d_summaries) {
+    const int n = d_todo ? n_todo : P;
+    if (n <= 0) return VX_OK;
+    if (!(sim->dt > 0.0)) return (set_error("SimConfig: dt must be > 0"), VX_EINVAL);
+    if (!(sim->duration >= 0.0)) return (set_error("SimConfig: duration must be >= 0"), VX_EINVAL);
+    if (!(sim->actuation_frequency > 0.0)) return (set_error("SimConfig: frequency must be > 0"), VX_EINVAL);
+    const int cells = w * h * d;
+    VX_TRY(ctx->eval_body.alloc(static_cast<size_t>(n) * cells));
+    VX_TRY(ctx->eval_summ.alloc(n));
+    VX_TRY(largest_component_dev(ctx, n, w, h, d, d_mat, ctx->eval_body.p, d_todo));
+    if (!ctx->eval_batch) ctx->eval_batch = new vx_batch;
+    vx_batch* b = ctx->eval_batch;
+    VX_TRY(build_batch_into(ctx, b, n, w, h, d, ctx->eval_body.p, d_weight, d_todo, table, plane));
+    VX_TRY(gate_dev(ctx, b));
+    const int64_t n_steps = std::llround(sim->duration / sim->dt);  // physics.hpp:295
+    VX_TRY(integrate(ctx, b, sim, 0, n_steps, false, nullptr, 0, ctx->eval_summ.p, nullptr));
+    return fitness_dev(ctx, n, d_todo, b->status.p, ctx->eval_summ.p, d_fitness, d_updates, d_summaries);
+}
+
+}  // namespace vx
+
+struct vx_evo {
+    vx_ctx* ctx = nullptr;
+    vx_evo_config cfg{};
+    vx_hyper params{};
+    int P = 0, cells = 0;
+    int64_t np = 0, nb = 0;
+    int cur = 0;
+    DevBuf<double> prm[2], bm[2], fit[2], gw[2];
+    DevBuf<uint8_t> ev[2], grid[2];
+    std::vector<uint8_t> h_eval, h_has_grid;
+    // generation scratch
+    DevBuf<int32_t> d_todo, d_dec, perm, iota;
+    DevBuf<double> xbuf, sorted, keys_tmp, stats, div;
+    DevBuf<int64_t> hist;
+    DevBuf<uint32_t> guard;
+    // breeding plan (host parse -> device)
+    DevBuf<ChildPlan> d_plan;
+    DevBuf<uint32_t> d_masks;
+    DevBuf<MutEntry> d_mut;
+    std::vector<ChildPlan> h_plan;
+    std::vector<uint32_t> h_masks;
+    std::vector<MutEntry> h_mut;
+    int64_t mask_words = 0;
+    int plan_elite = 0;
+    std::thread plan_thread;
+    bool plan_running = false;
+    std::mt19937_64 rng;
+    int generation = 0;
+    double best_fitness = 0.0;
+    bool has_best = false;
+    std::vector<double> best_genome;
+    // begin/finish
+    bool begun = false;
+    std::vector<int32_t> todo;
+    int rank = 0, world = 1;
+    std::chrono::steady_clock::time_point t0;
+    vx_materials table{};
+    double* ext_xbuf = nullptr;  // caller-owned exchange buffer (NCCL all-reduce operand)
+    double* xb() { return ext_xbuf ? ext_xbuf : xbuf.p; }
+
+    ~vx_evo() {
+        if (plan_thread.joinable()) plan_thread.join();
+    }
+};
+
+namespace {
+
+// Rng::uniform01 / normal / index (rng.hpp:23-39) on the GA stream.
+inline double u01(std::mt19937_64& r) { return static_cast<double>(r() >> 11) * 0x1.0p-53; }
+inline double normal(std::mt19937_64& r) {
+    const double u1 = (static_cast<double>(r() >> 11) + 0.5) * 0x1.0p-53;
+    const double u2 = static_cast<double>(r() >> 11) * 0x1.0p-53;
+    return std::sqrt(-2.0 * std::log(u1)) * std::cos(2.0 * M_PI * u2);
+}
+inline uint64_t index(std::mt19937_64& r, uint64_t n) {
+    const uint64_t threshold = (0 - n) % n;
+    for (;;) {
+        const uint64_t x = r();
+        if (x >= threshold) return x % n;
+    }
+}
+// tournament_select (evolution.hpp:169-173) -> sorted rank
+inline int32_t tournament(std::mt19937_64& r, int P, int size) {
+    uint64_t winner = index(r, static_cast<uint64_t>(P));
+    for (int k = 1; k < size; ++k) winner = std::min<uint64_t>(winner, index(r, static_cast<uint64_t>(P)));
+    return static_cast<int32_t>(winner);
+}
+
+// Breeding loop (evolution.hpp:267-289) in rank space: consumes the GA
+// stream draw-for-draw like the reference.
+void parse_plan(vx_evo* e) {
+    const int P = e->P;
+    const int n_elite = vx_elite_count(e->params.elite_fraction, P);
+    e->plan_elite = n_elite;
+    const int n_child = P - n_elite;
+    e->h_plan.resize(std::max(1, n_child));
+    e->h_masks.clear();
+    e->h_mut.clear();
+    int slots = 0;
+    const double cx_rate = e->params.crossover_rate, rate = e->params.mutation_rate, scale = e->params.mutation_scale;
+    for (int c = n_elite; c < P; ++c) {
+        ChildPlan& p = e->h_plan[c - n_elite];
+        p.pa = tournament(e->rng, P, e->cfg.tournament_size);
+        p.pb = -1;
+        p.mask_slot = -1;
+        p.pad = 0;
+        if (u01(e->rng) < cx_rate) {
+            p.pb = tournament(e->rng, P, e->cfg.tournament_size);
+            p.mask_slot = slots++;
+            const size_t base = e->h_masks.size();
+            e->h_masks.resize(base + e->mask_words, 0u);
+            uint32_t* m = e->h_masks.data() + base;
+            for (int64_t i = 0; i < e->np; ++i)  // crossover (evolution.hpp:143-155)
+                if (u01(e->rng) < 0.5) m[i >> 5] |= 1u << (i & 31);
+        }
+        for (int64_t i = 0; i < e->np; ++i)  // mutate (evolution.hpp:160-165)
+            if (u01(e->rng) < rate) e->h_mut.push_back(MutEntry{c, static_cast<int32_t>(i), normal(e->rng) * scale});
+    }
+}
+
+vx_status validate_cfg(const vx_evo_config* c) {
+    if (c->population < 2) return (set_error("EvolutionConfig: population must be >= 2"), VX_EINVAL);
+    if (c->generations < 0) return (set_error("EvolutionConfig: generations must be >= 0"), VX_EINVAL);
+    if (c->grid_w < 1 || c->grid_h < 1 || c->grid_d < 1)
+        return (set_error("EvolutionConfig: grid dimensions must be >= 1"), VX_EINVAL);
+    if (c->tournament_size < 1) return (set_error("EvolutionConfig: tournament size must be >= 1"), VX_EINVAL);
+    if (c->arch.m < 1) return (set_error("EncodingSpec: m must be >= 1"), VX_EINVAL);
+    if (!(c->arch.sigma > 0.0)) return (set_error("EncodingSpec: sigma must be > 0"), VX_EINVAL);
+    if (param_count(&c->arch) < 0) return (set_error("sample_genome: hidden widths must be >= 1"), VX_EINVAL);
+    if (!(c->sim.dt > 0.0)) return (set_error("SimConfig: dt must be > 0"), VX_EINVAL);
+    if (!(c->sim.duration >= 0.0)) return (set_error("SimConfig: duration must be >= 0"), VX_EINVAL);
+    if (!(c->sim.actuation_frequency > 0.0)) return (set_error("SimConfig: frequency must be > 0"), VX_EINVAL);
+    return VX_OK;
+}
+
+vx_status alloc_evo(vx_evo* e) {
+    const size_t P = static_cast<size_t>(e->P);
+    for (int s = 0; s < 2; ++s) {
+        VX_TRY(e->prm[s].alloc(P * e->np));
+        VX_TRY(e->bm[s].alloc(P * e->nb));
+        VX_TRY(e->fit[s].alloc(P));
+        VX_TRY(e->gw[s].alloc(P * e->cells));
+        VX_TRY(e->ev[s].alloc(P));
+        VX_TRY(e->grid[s].alloc(P * e->cells));
+    }
+    VX_TRY(e->d_todo.alloc(P));
+    VX_TRY(e->d_dec.alloc(P));
+    VX_TRY(e->perm.alloc(P));
+    VX_TRY(e->iota.alloc(P));
+    VX_TRY(e->xbuf.alloc(2 * P));
+    VX_TRY(e->sorted.alloc(P));
+    VX_TRY(e->keys_tmp.alloc(P));
+    VX_TRY(e->stats.alloc(4));
+    VX_TRY(e->div.alloc(1));
+    VX_TRY(e->hist.alloc(static_cast<size_t>(e->cells) * VX_NMAT));
+    VX_TRY(e->guard.alloc(1));
+    VX_TRY(e->d_plan.alloc(P));
+    e->mask_words = (e->np + 31) / 32;
+    e->h_eval.assign(P, 0);
+    e->h_has_grid.assign(P, 0);
+    return VX_OK;
+}
+
+void start_plan(vx_evo* e) {
+    e->plan_running = true;
+    e->plan_thread = std::thread([e] { parse_plan(e); });
+}
+
+void join_plan(vx_evo* e) {
+    if (e->plan_thread.joinable()) e->plan_thread.join();
+    e->plan_running = false;
+}
+
+}  // namespace
+
+extern "C" {
+
+vx_status vx_evo_create(vx_ctx* ctx, const vx_evo_config* cfg, vx_evo** out) {
+    if (!ctx || !cfg || !out) return VX_EINVAL;
+    VX_TRY(validate_cfg(cfg));
+    auto e = std::make_unique<vx_evo>();
+    e->ctx = ctx;
+    e->cfg = *cfg;
+    e->params = cfg->initial_params;
+    vx_hyper_clamp(&e->params);
+    e->P = cfg->population;
+    e->cells = cfg->grid_w * cfg->grid_h * cfg->grid_d;
+    e->np = param_count(&cfg->arch);
+    e->nb = 3LL * cfg->arch.m;
+    VX_TRY(alloc_evo(e.get()));
+    // init_evolution (evolution.hpp:197-211): per-genome seeds from the master
+    // stream, genomes sampled on device (K14)
+    e->rng.seed(cfg->seed);
+    std::vector<uint64_t> seeds(e->P);
+    for (auto& s : seeds) s = e->rng();
+    DevBuf<uint64_t> d_seeds;
+    VX_TRY(d_seeds.alloc(e->P));
+    VX_CUDA(cudaMemcpyAsync(d_seeds.p, seeds.data(), e->P * sizeof(uint64_t), cudaMemcpyHostToDevice, ctx->stream));
+    VX_TRY(sample_genomes_dev(ctx, &cfg->arch, e->P, d_seeds.p, e->prm[0].p, e->bm[0].p));
+    VX_CUDA(cudaMemsetAsync(e->fit[0].p, 0, e->P * sizeof(double), ctx->stream));
+    VX_CUDA(cudaMemsetAsync(e->ev[0].p, 0, e->P, ctx->stream));
+    VX_CUDA(cudaStreamSynchronize(ctx->stream));
+    *out = e.release();
+    return VX_OK;
+}
+
+vx_status vx_evo_free(vx_evo* e) {
+    if (e) {
+        join_plan(e);
+        if (e->ctx) cudaStreamSynchronize(e->ctx->stream);
+        delete e;
+    }
+    return VX_OK;
+}
+
+vx_status vx_evo_begin(vx_evo* e, int32_t rank, int32_t world) {
+    if (!e || world < 1 || rank < 0 || rank >= world) return VX_EINVAL;
+    if (e->begun) return (set_error("vx_evo_begin: generation already begun"), VX_ESTATE);
+    vx_ctx* ctx = e->ctx;
+    e->t0 = std::chrono::steady_clock::now();
+    e->rank = rank;
+    e->world = world;
+    const int c = e->cur;
+    // detail::scaled_materials (evolution.hpp:123-129, 229)
+    e->table = e->cfg.materials;
+    e->table.k_muscle *= e->params.material_multipliers[0];
+    e->table.k_soft *= e->params.material_multipliers[1];
+    e->table.k_bone *= e->params.material_multipliers[2];
+    // breeding plan parse overlaps everything below
+    start_plan(e);
+    // decode individuals without a cached grid (evolution.hpp:230-236)
+    std::vector<int32_t> dec;
+    e->todo.clear();
+    for (int a = 0; a < e->P; ++a) {
+        if (!e->h_has_grid[a]) dec.push_back(a);
+        if (!e->h_eval[a]) e->todo.push_back(a);
+    }
+    if (!dec.empty()) {
+        VX_CUDA(cudaMemcpyAsync(e->d_dec.p, dec.data(), dec.size() * sizeof(int32_t), cudaMemcpyHostToDevice,
+                                ctx->stream));
+        VX_TRY(decode_dev(ctx, &e->cfg.arch, e->P, e->prm[c].p, e->bm[c].p, e->cfg.grid_w, e->cfg.grid_h,
+                          e->cfg.grid_d, e->grid[c].p, e->gw[c].p, nullptr, e->d_dec.p, static_cast<int>(dec.size())));
+        for (int a : dec) e->h_has_grid[a] = 1;
+    }
+    // this rank's shard of the evaluations (strided over the todo list)
+    std::vector<int32_t> mine;
+    for (size_t q = rank; q < e->todo.size(); q += world) mine.push_back(e->todo[q]);
+    VX_CUDA(cudaMemsetAsync(e->xb(), 0, 2 * e->P * sizeof(double), ctx->stream));
+    if (!mine.empty()) {
+        VX_CUDA(cudaMemcpyAsync(e->d_todo.p, mine.data(), mine.size() * sizeof(int32_t), cudaMemcpyHostToDevice,
+                                ctx->stream));
+        VX_TRY(evaluate_pipeline(ctx, e->P, e->cfg.grid_w, e->cfg.grid_h, e->cfg.grid_d, e->grid[c].p, e->gw[c].p,
+                                 &e->table, &e->cfg.plane, &e->cfg.sim, e->d_todo.p, static_cast<int>(mine.size()),
+                                 e->xb(), e->xb() + e->P, nullptr));
+    }
+    // the todo list (all ranks) goes to the device for the merge
+    if (!e->todo.empty())
+        VX_CUDA(cudaMemcpyAsync(e->d_todo.p, e->todo.data(), e->todo.size() * sizeof(int32_t), cudaMemcpyHostToDevice,
+                                ctx->stream));
+    e->begun = true;
+    return VX_OK;
+}
+
+vx_status vx_evo_exchange_buffer(vx_evo* e, double** d_buf, int64_t* n_doubles) {
+    if (!e || !d_buf) return VX_EINVAL;
+    *d_buf = e->xb();
+    if (n_doubles) *n_doubles = 2LL * e->P;
+    return VX_OK;
+}
+
+vx_status vx_evo_set_exchange_buffer(vx_evo* e, double* d_buf) {
+    if (!e) return VX_EINVAL;
+    if (e->begun) return (set_error("exchange buffer change mid-generation"), VX_ESTATE);
+    e->ext_xbuf = d_buf;
+    return VX_OK;
+}
+
+vx_status vx_evo_load_population_dev(vx_evo* e, const double* d_params, const double* d_bmat) {
+    if (!e || !d_params || !d_bmat) return VX_EINVAL;
+    if (e->begun) return (set_error("population is mid-generation"), VX_ESTATE);
+    cudaStream_t s = e->ctx->stream;
+    const int c = e->cur;
+    const size_t P = e->P;
+    VX_CUDA(cudaMemcpyAsync(e->prm[c].p, d_params, P * e->np * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    VX_CUDA(cudaMemcpyAsync(e->bm[c].p, d_bmat, P * e->nb * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    VX_CUDA(cudaMemsetAsync(e->fit[c].p, 0, P * sizeof(double), s));
+    VX_CUDA(cudaMemsetAsync(e->ev[c].p, 0, P, s));
+    std::fill(e->h_eval.begin(), e->h_eval.end(), 0);
+    std::fill(e->h_has_grid.begin(), e->h_has_grid.end(), 0);
+    return VX_OK;
+}
+
+vx_status vx_evo_finish(vx_evo* e, vx_report* rep) {
+    if (!e) return VX_EINVAL;
+    if (!e->begun) return (set_error("vx_evo_finish without vx_evo_begin"), VX_ESTATE);
+    vx_ctx* ctx = e->ctx;
+    const int c = e->cur, nx = 1 - c, P = e->P;
+    VX_TRY(merge_dev(ctx, static_cast<int>(e->todo.size()), e->d_todo.p, e->xb(), e->fit[c].p, e->ev[c].p));
+    VX_TRY(sort_stats_dev(ctx, P, e->fit[c].p, e->perm.p, e->sorted.p, e->iota.p, e->keys_tmp.p, e->stats.p));
+    VX_TRY(histogram_dev(ctx, P, e->cells, e->grid[c].p, e->hist.p, false));
+    VX_TRY(diversity_from_hist_dev(ctx, P, e->cells, e->hist.p, e->div.p));
+    double st[3], div = 0.0;
+    std::vector<double> upd(e->todo.empty() ? 0 : P);
+    VX_CUDA(cudaMemcpyAsync(st, e->stats.p, 3 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    VX_CUDA(cudaMemcpyAsync(&div, e->div.p, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    if (!upd.empty())
+        VX_CUDA(cudaMemcpyAsync(upd.data(), e->xb() + P, P * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    int32_t top = 0;
+    VX_CUDA(cudaMemcpyAsync(&top, e->perm.p, sizeof(int32_t), cudaMemcpyDeviceToHost, ctx->stream));
+    VX_CUDA(cudaStreamSynchronize(ctx->stream));
+    // best_fitness / best_genome (evolution.hpp:246-249)
+    if (!e->has_best || st[0] > e->best_fitness) {
+        e->best_fitness = st[0];
+        e->best_genome.resize(e->np);
+        VX_CUDA(cudaMemcpy(e->best_genome.data(), e->prm[c].p + static_cast<size_t>(top) * e->np,
+                           e->np * sizeof(double), cudaMemcpyDeviceToHost));
+        e->has_best = true;
+    }
+    vx_report r{};
+    r.generation = e->generation;
+    r.params = e->params;
+    r.best = st[0];
+    r.mean = st[1];
+    r.stddev = st[2];
+    r.diversity = div;
+    r.evaluations = static_cast<int32_t>(e->todo.size());
+    uint64_t total = 0;
+    for (int32_t a : e->todo) total += static_cast<uint64_t>(upd[a]);
+    r.spring_updates = total;
+    // breed (evolution.hpp:267-289)
+    join_plan(e);
+    const int n_elite = e->plan_elite;
+    const int n_child = P - n_elite;
+    VX_TRY(e->d_plan.alloc(std::max(1, n_child)));
+    VX_TRY(e->d_masks.alloc(std::max<size_t>(1, e->h_masks.size())));
+    VX_TRY(e->d_mut.alloc(std::max<size_t>(1, e->h_mut.size())));
+    if (n_child > 0)
+        VX_CUDA(cudaMemcpyAsync(e->d_plan.p, e->h_plan.data(), n_child * sizeof(ChildPlan), cudaMemcpyHostToDevice,
+                                ctx->stream));
+    if (!e->h_masks.empty())
+        VX_CUDA(cudaMemcpyAsync(e->d_masks.p, e->h_masks.data(), e->h_masks.size() * sizeof(uint32_t),
+                                cudaMemcpyHostToDevice, ctx->stream));
+    if (!e->h_mut.empty())
+        VX_CUDA(cudaMemcpyAsync(e->d_mut.p, e->h_mut.data(), e->h_mut.size() * sizeof(MutEntry),
+                                cudaMemcpyHostToDevice, ctx->stream));
+    BreedArgs A{};
+    A.n_elite = n_elite;
+    A.np = e->np;
+    A.nb = e->nb;
+    A.cells = e->cells;
+    A.mask_words = e->mask_words;
+    A.perm = e->perm.p;
+    A.plan = e->d_plan.p;
+    A.masks = e->d_masks.p;
+    A.src_params = e->prm[c].p;
+    A.src_bmat = e->bm[c].p;
+    A.src_fit = e->fit[c].p;
+    A.src_eval = e->ev[c].p;
+    A.src_grid = e->grid[c].p;
+    A.src_gridw = e->gw[c].p;
+    A.dst_params = e->prm[nx].p;
+    A.dst_bmat = e->bm[nx].p;
+    A.dst_fit = e->fit[nx].p;
+    A.dst_eval = e->ev[nx].p;
+    A.dst_grid = e->grid[nx].p;
+    A.dst_gridw = e->gw[nx].p;
+    VX_TRY(breed_dev(ctx, A, P, e->d_mut.p, static_cast<int64_t>(e->h_mut.size())));
+    // host mirrors: elites are evaluated and keep their grids; children are fresh
+    for (int a = 0; a < P; ++a) {
+        e->h_eval[a] = a < n_elite ? 1 : 0;
+        e->h_has_grid[a] = a < n_elite ? 1 : 0;
+    }
+    e->cur = nx;
+    ++e->generation;
+    e->begun = false;
+    VX_CUDA(cudaStreamSynchronize(ctx->stream));  // host plan buffers are reused next generation
+    r.wall_time = std::chrono::duration<double>(std::chrono::steady_clock::now() - e->t0).count();
+    if (rep) *rep = r;
+    return VX_OK;
+}
+
+vx_status vx_evo_generation(vx_evo* e, vx_report* rep) {
+    VX_TRY(vx_evo_begin(e, 0, 1));
+    return vx_evo_finish(e, rep);
+}
+
+vx_status vx_evo_get_population(vx_evo* e, double* params, double* bmat, double* fitness, uint8_t* evaluated,
+                                uint8_t* grids, double* grid_w) {
+    if (!e) return VX_EINVAL;
+    if (e->begun) return (set_error("population is mid-generation"), VX_ESTATE);
+    const int c = e->cur;
+    const size_t P = e->P;
+    cudaStream_t s = e->ctx->stream;
+    if (params) VX_CUDA(cudaMemcpyAsync(params, e->prm[c].p, P * e->np * sizeof(double), cudaMemcpyDeviceToHost, s));
+    if (bmat) VX_CUDA(cudaMemcpyAsync(bmat, e->bm[c].p, P * e->nb * sizeof(double), cudaMemcpyDeviceToHost, s));
+    if (fitness) VX_CUDA(cudaMemcpyAsync(fitness, e->fit[c].p, P * sizeof(double), cudaMemcpyDeviceToHost, s));
+    if (evaluated) VX_CUDA(cudaMemcpyAsync(evaluated, e->ev[c].p, P, cudaMemcpyDeviceToHost, s));
+    if (grids) VX_CUDA(cudaMemcpyAsync(grids, e->grid[c].p, P * e->cells, cudaMemcpyDeviceToHost, s));
+    if (grid_w) VX_CUDA(cudaMemcpyAsync(grid_w, e->gw[c].p, P * e->cells * sizeof(double), cudaMemcpyDeviceToHost, s));
+    VX_CUDA(cudaStreamSynchronize(s));
+    for (size_t a = 0; a < P; ++a)
+        if (!e->h_has_grid[a]) {
+            if (grids) std::memset(grids + a * e->cells, 255, e->cells);
+            if (grid_w) std::fill(grid_w + a * e->cells, grid_w + (a + 1) * e->cells, 0.0);
+        }
+    return VX_OK;
+}
+
+vx_status vx_evo_set_population(vx_evo* e, const double* params, const double* bmat, const double* fitness,
+                                const uint8_t* evaluated, const uint8_t* grids, const double* grid_w) {
+    if (!e || !params || !bmat) return VX_EINVAL;
+    if (e->begun) return (set_error("population is mid-generation"), VX_ESTATE);
+    const int c = e->cur;
+    const size_t P = e->P;
+    cudaStream_t s = e->ctx->stream;
+    VX_CUDA(cudaMemcpyAsync(e->prm[c].p, params, P * e->np * sizeof(double), cudaMemcpyHostToDevice, s));
+    VX_CUDA(cudaMemcpyAsync(e->bm[c].p, bmat, P * e->nb * sizeof(double), cudaMemcpyHostToDevice, s));
+    std::vector<double> f(P, 0.0);
+    std::vector<uint8_t> ev(P, 0);
+    if (fitness) std::copy(fitness, fitness + P, f.begin());
+    if (evaluated) std::copy(evaluated, evaluated + P, ev.begin());
+    VX_CUDA(cudaMemcpyAsync(e->fit[c].p, f.data(), P * sizeof(double), cudaMemcpyHostToDevice, s));
+    VX_CUDA(cudaMemcpyAsync(e->ev[c].p, ev.data(), P, cudaMemcpyHostToDevice, s));
+    std::vector<double> gw;
+    if (grids) {
+        VX_CUDA(cudaMemcpyAsync(e->grid[c].p, grids, P * e->cells, cudaMemcpyHostToDevice, s));
+        if (!grid_w) gw.assign(P * e->cells, 1.0);
+        VX_CUDA(cudaMemcpyAsync(e->gw[c].p, grid_w ? grid_w : gw.data(), P * e->cells * sizeof(double),
+                                cudaMemcpyHostToDevice, s));
+    }
+    VX_CUDA(cudaStreamSynchronize(s));
+    for (size_t a = 0; a < P; ++a) {
+        e->h_eval[a] = ev[a] ? 1 : 0;
+        e->h_has_grid[a] = grids ? 1 : 0;
+    }
+    return VX_OK;
+}
+
+vx_status vx_evo_population_dev(vx_evo* e, double** d_params, double** d_bmat, double** d_fitness) {
+    if (!e) return VX_EINVAL;
+    if (d_params) *d_params = e->prm[e->cur].p;
+    if (d_bmat) *d_bmat = e->bm[e->cur].p;
+    if (d_fitness) *d_fitness = e->fit[e->cur].p;
+    return VX_OK;
+}
+
+int64_t vx_evo_rng_state(vx_evo* e, char* buf, int64_t cap) {
+    if (!e) return -1;
+    if (e->plan_running) join_plan(e);
+    std::ostringstream os;
+    os << e->rng;
+    const std::string s = os.str();
+    if (buf && cap > 0) {
+        std::strncpy(buf, s.c_str(), static_cast<size_t>(cap - 1));
+        buf[cap - 1] = 0;
+    }
+    return static_cast<int64_t>(s.size());
+}
+
+vx_status vx_evo_set_rng_state(vx_evo* e, const char* state) {
+    if (!e || !state) return VX_EINVAL;
+    if (e->begun) return (set_error("rng state change mid-generation"), VX_ESTATE);
+    std::istringstream is(state);
+    std::mt19937_64 r;
+    is >> r;
+    if (is.fail()) return (set_error("invalid mt19937_64 state text"), VX_EINVAL);
+    e->rng = r;
+    return VX_OK;
+}
+
+vx_status vx_evo_get_params(vx_evo* e, vx_hyper* h) {
+    if (!e || !h) return VX_EINVAL;
+    *h = e->params;
+    return VX_OK;
+}
+
+vx_status vx_evo_set_params(vx_evo* e, const vx_hyper* h) {
+    if (!e || !h) return VX_EINVAL;
+    if (e->begun) return (set_error("params change mid-generation"), VX_ESTATE);
+    e->params = *h;
+    vx_hyper_clamp(&e->params);  // evolution.hpp:224-225
+    return VX_OK;
+}
+
+int32_t vx_evo_generation_index(vx_evo* e) { return e ? e->generation : -1; }
+
+int32_t vx_evo_best(vx_evo* e, double* best_fitness, double* best_params) {
+    if (!e) return 0;
+    if (best_fitness) *best_fitness = e->best_fitness;
+    if (!e->has_best) return 0;
+    if (best_params) std::copy(e->best_genome.begin(), e->best_genome.end(), best_params);
+    return 1;
+}
+
+}  // extern "C"
