@@ -116,6 +116,8 @@ struct BuildArgs {
     double* sign;
     double* amp;
     double* phase;
+    int32_t* vkey;     // per mass: vertex key x + vw*(y + vh*z)
+    int16_t* act_vox;  // per spring: actuating voxel (lowest-index muscle) or -1
 };
 
 // forward lattice offsets (dz, dy, dx), ascending key offset (see header)
@@ -232,6 +234,7 @@ __global__ void __launch_bounds__(kThreads) build_kernel(BuildArgs A) {
             A.vel[1 * A.M + mo + a] = 0.0;
             A.vel[2 * A.M + mo + a] = 0.0;
             A.mass[mo + a] = A.table.mass_per_vertex;
+            A.vkey[mo + a] = v;
             for (int q = 0; q < 13; ++q) {
                 const int dz = c_fwd[q][0], dy = c_fwd[q][1], dx = c_fwd[q][2];
                 const int ux = x + dx, uy = y + dy, uz = z + dz;
@@ -271,7 +274,7 @@ __global__ void __launch_bounds__(kThreads) build_kernel(BuildArgs A) {
             const int z0 = dz == 0 ? z - 1 : (dz > 0 ? z : z - 1), z1 = dz == 0 ? z : z0;
             double k_sum = 0.0;
             int count = 0;
-            int act_mat = 0;
+            int act_mat = 0, act_ci = -1;
             double act_w = 0.0;
             // ascending voxel linear index: z, then y, then x
             for (int cz = z0; cz <= z1; ++cz)
@@ -286,6 +289,7 @@ __global__ void __launch_bounds__(kThreads) build_kernel(BuildArgs A) {
                         if ((m == 1 || m == 2) && act_mat == 0) {
                             act_mat = m;
                             act_w = s_wt[ci];
+                            act_ci = ci;
                         }
                     }
             if (count == 0) continue;
@@ -300,6 +304,7 @@ __global__ void __launch_bounds__(kThreads) build_kernel(BuildArgs A) {
             A.sign[q_out] = act_mat == 1 ? 1.0 : (act_mat == 2 ? -1.0 : 0.0);
             A.amp[q_out] = act_mat ? act_w * A.table.amp_max : 0.0;
             A.phase[q_out] = act_mat ? act_w * A.table.phase_max : 0.0;
+            A.act_vox[q_out] = static_cast<int16_t>(act_ci);
             ++q_out;
         }
     }
@@ -384,6 +389,14 @@ vx_status build_batch_into(vx_ctx* ctx, vx_batch* b, int n, int w, int h, int d,
     A.sign = b->sign.p;
     A.amp = b->amp.p;
     A.phase = b->phase.p;
+    VX_TRY(b->vkey.alloc(b->M));
+    VX_TRY(b->act_vox.alloc(b->S));
+    A.vkey = b->vkey.p;
+    A.act_vox = b->act_vox.p;
+    b->lattice = true;
+    b->lw = w;
+    b->lh = h;
+    b->ld = d;
     const int ncell = w * h * d;
     const size_t smem = static_cast<size_t>(ncell) * (sizeof(double) + 1) + 2ull * nm_cap * sizeof(int) + 16;
     if (smem > ctx->smem_optin) return (set_error("build: grid too large for one CTA"), VX_EINVAL);

@@ -312,6 +312,28 @@ vx_status integrate(vx_ctx* ctx, vx_batch* b, const vx_sim* sim, int64_t k0, int
     if (grid <= 0) return VX_OK;
     VX_TRY(ensure_drive(ctx, sim->actuation_frequency, sim->dt, k0, n_steps > 0 ? n_steps : 1));
 
+    if (!d_robot_list && !d_summary_slot && lattice_applicable(ctx, b)) {
+        const SimParams sp{sim->gravity, sim->dt, sim->enable_gravity, sim->enable_contact, b->plane.k,
+                           b->plane.mu_static, b->plane.mu_kinetic};
+        std::pair<cudaEvent_t, cudaEvent_t> ev{nullptr, nullptr};
+        if (ctx->timing) {
+            if (ctx->event_pool.empty()) {
+                VX_CUDA(cudaEventCreate(&ev.first));
+                VX_CUDA(cudaEventCreate(&ev.second));
+            } else {
+                ev = ctx->event_pool.back();
+                ctx->event_pool.pop_back();
+            }
+            VX_CUDA(cudaEventRecord(ev.first, ctx->stream));
+        }
+        VX_TRY(integrate_lattice(ctx, b, sim, n_steps, write_back, d_summaries, sp));
+        if (ctx->timing) {
+            VX_CUDA(cudaEventRecord(ev.second, ctx->stream));
+            ctx->pending.push_back(ev);
+        }
+        return VX_OK;
+    }
+
     KernelArgs A{};
     A.b = view_of(b);
     A.drive = ctx->drive.p;
