@@ -690,6 +690,12 @@ class EvolutionState:
         return rep
 
 
+def shard_indices(todo: Sequence[int], rank: int, world: int) -> list:
+    """The children a rank evaluates in vx_evo_begin(rank, world): a strided
+    split of the generation's todo list (every index exactly once)."""
+    return [int(t) for t in list(todo)[rank::world]]
+
+
 def init_evolution(config: EvolutionConfig, ctx: Optional[Context] = None) -> EvolutionState:
     return EvolutionState(config, ctx)
 
