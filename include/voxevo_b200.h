@@ -284,6 +284,11 @@ vx_status vx_integrator_timing(vx_ctx* ctx, double* total_ms, int64_t* n_launche
 /* Measured FP64 FMA throughput of the device (TFLOP/s, 2 flops per DFMA),
  * the denominator for the FP64-issue-bound integrator's roofline. */
 vx_status vx_fp64_peak(vx_ctx* ctx, double* tflops);
+/* Self-check of the integrator's branch-free sqrt / reciprocal against the
+ * IEEE sqrt(x) and 1.0/x over n pseudo-random inputs spanning the ranges the
+ * integrator feeds them (plus powers of two and their neighbours);
+ * mismatches[0] = sqrt, mismatches[1] = rcp. */
+vx_status vx_fastmath_check(vx_ctx* ctx, int64_t n, uint64_t seed, int64_t* mismatches);
 
 /* ------------------------------------------------------------- bench ---- */
 /* run_bench (bench.hpp:50-86): `jobs` copies of bench_robot(grid) stepped

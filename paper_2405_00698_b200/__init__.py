@@ -267,6 +267,7 @@ def _declare(lib):
         "vx_timing_enable": (i32, [vp, i32]),
         "vx_integrator_timing": (i32, [vp, P(dbl), P(i64), i32]),
         "vx_fp64_peak": (i32, [vp, P(dbl)]),
+        "vx_fastmath_check": (i32, [vp, i64, u64, vp]),
     }
     for name, (res, args) in sigs.items():
         fn = getattr(lib, name)
@@ -359,6 +360,12 @@ class Context:
         t = C.c_double()
         _check(_lib().vx_fp64_peak(self.h, C.byref(t)))
         return float(t.value)
+
+    def fastmath_check(self, n: int, seed: int = 1) -> tuple:
+        """Mismatches (sqrt, rcp) of the integrator's branch-free sqrt/rcp vs IEEE over n samples."""
+        out = np.zeros(2, np.int64)
+        _check(_lib().vx_fastmath_check(self.h, n, seed, out.ctypes.data))
+        return int(out[0]), int(out[1])
 
     def info(self) -> dict:
         sm, clk = C.c_int32(), C.c_int32()

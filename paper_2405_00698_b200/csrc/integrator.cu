@@ -77,7 +77,7 @@ __global__ void __launch_bounds__(kThreads) integrate_kernel(KernelArgs A) {
         X = sm;
         sm += 6 * nm;
     } else {
-        X = A.g_state + static_cast<size_t>(blockIdx.x) * 6 * A.nm_max;
+        X = A.g_state + static_cast<size_t>(blockIdx.x) * 10 * A.nm_max;
     }
     double* F;  // [fx(ns) fy(ns) fz(ns)]
     if (kForceSmem) {
@@ -87,11 +87,12 @@ __global__ void __launch_bounds__(kThreads) integrate_kernel(KernelArgs A) {
         F = A.g_force + static_cast<size_t>(blockIdx.x) * 3 * A.ns_max;
     }
     // per-mass constants (same bits as recomputing them every step)
-    double* MG = sm;         // m * g            (physics.hpp:226)
-    double* IMDT = sm + nm;  // dt / m           (physics.hpp:249)
-    double* GD = sm + 2 * nm;  // ground damping (physics.hpp:163-164)
-    double* MASS = sm + 3 * nm;
-    sm += 4 * nm;
+    double* MC = kStateSmem ? sm : A.g_state + static_cast<size_t>(blockIdx.x) * 10 * A.nm_max + 6 * A.nm_max;
+    double* MG = MC;           // m * g            (physics.hpp:226)
+    double* IMDT = MC + nm;    // dt / m           (physics.hpp:249)
+    double* GD = MC + 2 * nm;  // ground damping   (physics.hpp:163-164)
+    double* MASS = MC + 3 * nm;
+    if (kStateSmem) sm += 4 * nm;
     __shared__ int s_flag;
     __shared__ double s_maxsq[kThreads / 32];
 
@@ -354,10 +355,9 @@ vx_status integrate(vx_ctx* ctx, vx_batch* b, const vx_sim* sim, int64_t k0, int
     bool state_smem = true, force_smem = true;
     if (state_b + force_b + mconst_b > budget) force_smem = false;
     if (state_b + mconst_b > budget) state_smem = false;
-    if (!state_smem && mconst_b > budget) return (set_error("robot too large for the integrator"), VX_EINVAL);
-    size_t smem = mconst_b + (state_smem ? state_b : 0) + (force_smem ? force_b : 0);
+    size_t smem = (state_smem ? state_b + mconst_b : 0) + (force_smem ? force_b : 0);
     if (!state_smem) {
-        VX_TRY(ctx->scratch_state.alloc(static_cast<size_t>(grid) * 6 * b->nm_max));
+        VX_TRY(ctx->scratch_state.alloc(static_cast<size_t>(grid) * 10 * b->nm_max));
         A.g_state = ctx->scratch_state.p;
     }
     if (!force_smem) {

@@ -48,6 +48,7 @@ struct LatArgs {
     vx_summary* out;
     int nmp;  // masses per group, multiple of 32
     int vw, vh, nv, ncell;
+    double zero_len2;  // smallest len^2 whose IEEE sqrt is >= kZeroLengthEps
 };
 
 __device__ void com_seq(const double* X, int nmp, const double* mass, int nm, double* com) {
@@ -208,31 +209,52 @@ __global__ void __launch_bounds__(NMP, 1) lattice_kernel(LatArgs A) {
         // sqrt/div fast paths) and no store; a passive spring uses the dummy
         // voxel (SA = 0), so rest = rest0 + (0*rest0)*D == rest0 exactly, as in
         // the reference (amp_rest = 0, physics.hpp:157-159).
+        // The slots are computed in chunks whose results stay in registers
+        // until the chunk's stores: without an intervening shared-memory store
+        // the scheduler can overlap the loads and FP64 chains of independent
+        // springs (it cannot prove F does not alias X).
         int zero_len = 0;
+        const double* __restrict__ Xr = X;
+        constexpr int kChunk = 5;
 #pragma unroll
-        for (int d = 0; d < 13; ++d) {
-            const bool valid = (fmask >> d) & 1u;
-            const int nb = static_cast<int>(pnb[d] & 0xFFFFu);
-            const int vox = static_cast<int>(pnb[d] >> 16);
-            double dx = X[nb] - x0;
-            double dy = X[NMP + nb] - x1;
-            double dz = X[2 * NMP + nb] - x2;
-            dx = valid ? dx : 1.0;
-            dy = valid ? dy : 0.0;
-            dz = valid ? dz : 0.0;
-            const double len = sqrt(dx * dx + dy * dy + dz * dz);
-            zero_len |= (valid && len < kZeroLengthEps) ? 1 : 0;
-            const double r0 = PR[d * NMP + a];
-            const double rest = r0 + (SA[vox] * r0) * D[vox];
-            const double inv_len = 1.0 / len;
-            const double nx = dx * inv_len, ny = dy * inv_len, nz = dz * inv_len;
-            const double rel =
-                (X[3 * NMP + nb] - v0) * nx + (X[4 * NMP + nb] - v1) * ny + (X[5 * NMP + nb] - v2) * nz;
-            const double mag = pk[d] * (len - rest) + PC[d * NMP + a] * rel;
-            if (valid) {
-                F[(3 * d) * NMP + a] = mag * nx;
-                F[(3 * d + 1) * NMP + a] = mag * ny;
-                F[(3 * d + 2) * NMP + a] = mag * nz;
+        for (int c0 = 0; c0 < 13; c0 += kChunk) {
+            double ofx[kChunk], ofy[kChunk], ofz[kChunk];
+#pragma unroll
+            for (int q = 0; q < kChunk; ++q) {
+                const int d = c0 + q;
+                if (d >= 13) break;
+                const bool valid = (fmask >> d) & 1u;
+                const int nb = static_cast<int>(pnb[d] & 0xFFFFu);
+                const int vox = static_cast<int>(pnb[d] >> 16);
+                double dx = Xr[nb] - x0;
+                double dy = Xr[NMP + nb] - x1;
+                double dz = Xr[2 * NMP + nb] - x2;
+                dx = valid ? dx : 1.0;
+                dy = valid ? dy : 0.0;
+                dz = valid ? dz : 0.0;
+                const double len2 = dx * dx + dy * dy + dz * dz;
+                const double len = sqrt_rn_fast(len2);  // == sqrt(len2) on every used step (vx_internal.cuh)
+                zero_len |= (valid && len2 < A.zero_len2) ? 1 : 0;  // <=> sqrt(len2) < kZeroLengthEps
+                const double r0 = PR[d * NMP + a];
+                const double rest = r0 + (SA[vox] * r0) * D[vox];
+                const double inv_len = rcp_rn_fast(len);
+                const double nx = dx * inv_len, ny = dy * inv_len, nz = dz * inv_len;
+                const double rel = (Xr[3 * NMP + nb] - v0) * nx + (Xr[4 * NMP + nb] - v1) * ny +
+                                   (Xr[5 * NMP + nb] - v2) * nz;
+                const double mag = pk[d] * (len - rest) + PC[d * NMP + a] * rel;
+                ofx[q] = mag * nx;
+                ofy[q] = mag * ny;
+                ofz[q] = mag * nz;
+            }
+#pragma unroll
+            for (int q = 0; q < kChunk; ++q) {
+                const int d = c0 + q;
+                if (d >= 13) break;
+                if ((fmask >> d) & 1u) {
+                    F[(3 * d) * NMP + a] = ofx[q];
+                    F[(3 * d + 1) * NMP + a] = ofy[q];
+                    F[(3 * d + 2) * NMP + a] = ofz[q];
+                }
             }
         }
         ++steps;
@@ -385,6 +407,13 @@ vx_status integrate_lattice(vx_ctx* ctx, vx_batch* b, const vx_sim* sim, int64_t
     A.vh = b->lh + 1;
     A.nv = (b->lw + 1) * (b->lh + 1) * (b->ld + 1);
     A.ncell = b->lw * b->lh * b->ld;
+    {   // sqrt is monotone and correctly rounded (host and device alike), so
+        // len < eps  <=>  len^2 < T with T the smallest double whose sqrt >= eps
+        double t = kZeroLengthEps * kZeroLengthEps;
+        while (std::sqrt(t) >= kZeroLengthEps) t = std::nextafter(t, 0.0);
+        while (std::sqrt(t) < kZeroLengthEps) t = std::nextafter(t, 1.0);
+        A.zero_len2 = t;
+    }
     const size_t smem = lattice_smem(A.nmp, A.ncell);
     auto launch = [&](auto kernel, int threads) -> vx_status {
         VX_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));

@@ -24,9 +24,56 @@ __global__ void __launch_bounds__(256) dfma_kernel(double* out, int iters, doubl
     if (s == 12345.678) out[blockIdx.x] = s;  // keep the chains alive
 }
 
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+    z += 0x9E3779B97F4A7C15ULL;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+
+// x = 2^e * (1 + m), e uniform over [emin, emax], m a random 52-bit mantissa;
+// every 16th sample is a power of two or its neighbour (rounding corners).
+__device__ double sample_range(uint64_t h, int emin, int emax) {
+    const int e = emin + static_cast<int>((h >> 52) % static_cast<uint64_t>(emax - emin + 1));
+    uint64_t mant = h & 0xFFFFFFFFFFFFFULL;
+    if ((h & 0xF0000000000000ULL) == 0) mant = (h & 1) ? 0 : 0xFFFFFFFFFFFFFULL;
+    const uint64_t bits = (static_cast<uint64_t>(e + 1023) << 52) | mant;
+    return __longlong_as_double(static_cast<long long>(bits));
+}
+
+__global__ void fastmath_kernel(int64_t n, uint64_t seed, unsigned long long* bad) {
+    unsigned long long bs = 0, br = 0;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const uint64_t h = mix64(seed ^ static_cast<uint64_t>(i));
+        const double s = sample_range(h, -61, 44);          // spring length^2: [1e-18, 1e13]
+        const double x = sample_range(mix64(h), -31, 22);   // spring length: [1e-9, 4e6]
+        if (__double_as_longlong(sqrt_rn_fast(s)) != __double_as_longlong(sqrt(s))) ++bs;
+        if (__double_as_longlong(rcp_rn_fast(x)) != __double_as_longlong(1.0 / x)) ++br;
+    }
+    if (bs) atomicAdd(bad, bs);
+    if (br) atomicAdd(bad + 1, br);
+}
+
 }  // namespace
 
 extern "C" {
+
+vx_status vx_fastmath_check(vx_ctx* ctx, int64_t n, uint64_t seed, int64_t* mismatches) {
+    if (!ctx || !mismatches || n < 0) return VX_EINVAL;
+    DevBuf<unsigned long long> bad;
+    VX_TRY(bad.alloc(2));
+    VX_TRY(bad.zero(ctx->stream));
+    fastmath_kernel<<<ctx->sm_count * 8, 256, 0, ctx->stream>>>(n, seed, bad.p);
+    ctx->launches++;
+    VX_CUDA(cudaGetLastError());
+    unsigned long long h[2];
+    VX_CUDA(cudaMemcpyAsync(h, bad.p, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+    VX_CUDA(cudaStreamSynchronize(ctx->stream));
+    mismatches[0] = static_cast<int64_t>(h[0]);
+    mismatches[1] = static_cast<int64_t>(h[1]);
+    return VX_OK;
+}
 
 vx_status vx_timing_enable(vx_ctx* ctx, int32_t on) {
     if (!ctx) return VX_EINVAL;
