@@ -7,17 +7,21 @@
 //    a compile-time constant so every shared-memory address is an immediate
 //    offset.  A lattice spring (i, j) joins vertex i to i + off_d for one of 13
 //    "forward" directions d (ascending key offset == ascending j, i.e. the
-//    reference's (i, j) spring order).  Thread a owns the <= 13 forward springs
-//    of mass a and keeps their k / rest0 / c / neighbour / actuating voxel, its
-//    backward neighbours and its per-mass constants in REGISTERS for the whole
-//    launch, and its own mass state in registers across the step;
-//  * phase 1 writes the force on endpoint i of spring (a, a+off_d) to the
-//    direction-major slot F[d][a] — neighbour loads and slot stores of a warp
-//    touch consecutive addresses (no bank conflicts);
-//  * phase 2: mass a sums its backward slots F[d][b(a,d)] for d = 12..0
-//    (ascending i) then its forward slots F[d][a] for d = 0..12 (ascending j):
-//    exactly the reference's ascending-spring-index CSR order
-//    (physics.hpp:166-184, 219-225), then gravity / contact / integrate; the
+//    reference's (i, j) spring order).  Thread a owns the <= 13 BACKWARD
+//    springs (a - off_d, a) of mass a (it is their higher endpoint) and keeps
+//    their k / neighbour / actuating voxel, its forward neighbours and its
+//    per-mass constants in REGISTERS for the whole launch (rest0 and c in
+//    direction-major shared memory), its own mass state in registers;
+//  * phase 1 computes those springs for d = 12..0 (= ascending i = ascending
+//    spring index): the reference's ordered gather for mass a begins with
+//    exactly these terms (fx = 0.0; fx += (-1)*F_s), so thread a accumulates
+//    them in registers as it goes and stores each force ONCE, to the
+//    direction-major slot F[d][a], for the lower endpoint — neighbour loads
+//    and slot stores of a warp touch consecutive addresses (no conflicts);
+//  * phase 2 continues mass a's sum with its forward springs d = 0..12
+//    (ascending j), reading F[d][a + off_d] — completing the reference's
+//    ascending-spring-index CSR order (physics.hpp:166-184, 219-225) — then
+//    gravity / contact / integrate; the
 //    per-voxel drive D_v = sin(wt)cos(phi_v) + cos(wt)sin(phi_v) of the next
 //    step is evaluated once per voxel (every spring actuated by voxel v shares
 //    it, so amp_rest*D_v is the reference's
@@ -124,8 +128,8 @@ __global__ void __launch_bounds__(NMP, 1) lattice_kernel(LatArgs A) {
         }
     }
     double pk[13];
-    uint32_t pnb[13];  // forward neighbour | actuating voxel << 16 (ncell = passive/missing)
-    uint32_t bnb[7];   // backward neighbours, two u16 per word
+    uint32_t pnb[13];  // backward (lower) neighbour | actuating voxel << 16 (ncell = passive/missing)
+    uint32_t fnb[7];   // forward (higher) neighbours, two u16 per word
     unsigned fmask = 0u, bmask = 0u;
     double mg = 0.0, imdt = 0.0, gdmp = 0.0;
     double x0 = 0.0, x1 = 0.0, x2 = 0.0, v0 = 0.0, v1 = 0.0, v2 = 0.0;
@@ -137,7 +141,7 @@ __global__ void __launch_bounds__(NMP, 1) lattice_kernel(LatArgs A) {
         PC[d * NMP + a] = 0.0;
     }
 #pragma unroll
-    for (int q = 0; q < 7; ++q) bnb[q] = 0u;
+    for (int q = 0; q < 7; ++q) fnb[q] = 0u;
     if (live) {
         x0 = b.pos[mo + a];
         x1 = b.pos[b.M + mo + a];
@@ -172,16 +176,16 @@ __global__ void __launch_bounds__(NMP, 1) lattice_kernel(LatArgs A) {
 #pragma unroll
             for (int d = 0; d < 13; ++d) {
                 if (d == dd) {
-                    if (L > 0) {
-                        fmask |= 1u << d;
+                    if (L < 0) {  // spring (other, a): a is its higher endpoint and computes it
+                        bmask |= 1u << d;
                         pk[d] = b.k[so + s];
                         PR[d * NMP + a] = b.rest0[so + s];
                         PC[d * NMP + a] = b.c[so + s];
                         const int av = A.act_vox[so + s];
                         pnb[d] = static_cast<uint32_t>(other) | (static_cast<uint32_t>(av >= 0 ? av : A.ncell) << 16);
-                    } else {
-                        bmask |= 1u << d;
-                        bnb[d >> 1] |= static_cast<uint32_t>(other) << (16 * (d & 1));
+                    } else {      // spring (a, other): computed by `other`, read back in phase 2
+                        fmask |= 1u << d;
+                        fnb[d >> 1] |= static_cast<uint32_t>(other) << (16 * (d & 1));
                     }
                 }
             }
@@ -209,26 +213,32 @@ __global__ void __launch_bounds__(NMP, 1) lattice_kernel(LatArgs A) {
         // sqrt/div fast paths) and no store; a passive spring uses the dummy
         // voxel (SA = 0), so rest = rest0 + (0*rest0)*D == rest0 exactly, as in
         // the reference (amp_rest = 0, physics.hpp:157-159).
-        // The slots are computed in chunks whose results stay in registers
-        // until the chunk's stores: without an intervening shared-memory store
-        // the scheduler can overlap the loads and FP64 chains of independent
-        // springs (it cannot prove F does not alias X).
+        // Thread a computes its BACKWARD springs (i = lower neighbour, j = a),
+        // d = 12..0 = ascending i = ascending spring index, which is exactly
+        // the head of the reference's ordered gather for mass a
+        // (physics.hpp:219-225): fx starts at 0.0 and adds (-1)*F_s in that
+        // order, so the partial sums are accumulated here, in registers, and
+        // each force is stored once (slot F[d][a]) for its lower endpoint's
+        // forward pass.  Chunks keep independent springs overlapping: results
+        // stay in registers until the chunk's ordered adds and stores.
         int zero_len = 0;
+        double sx = 0.0, sy = 0.0, sz = 0.0;
         const double* __restrict__ Xr = X;
         constexpr int kChunk = 5;
 #pragma unroll
-        for (int c0 = 0; c0 < 13; c0 += kChunk) {
+        for (int c0 = 12; c0 >= 0; c0 -= kChunk) {
             double ofx[kChunk], ofy[kChunk], ofz[kChunk];
 #pragma unroll
             for (int q = 0; q < kChunk; ++q) {
-                const int d = c0 + q;
-                if (d >= 13) break;
-                const bool valid = (fmask >> d) & 1u;
+                const int d = c0 - q;
+                if (d < 0) break;
+                const bool valid = (bmask >> d) & 1u;
                 const int nb = static_cast<int>(pnb[d] & 0xFFFFu);
                 const int vox = static_cast<int>(pnb[d] >> 16);
-                double dx = Xr[nb] - x0;
-                double dy = Xr[NMP + nb] - x1;
-                double dz = Xr[2 * NMP + nb] - x2;
+                // spring_force_on_i with i = nb, j = a (physics.hpp:55-64, 201-212)
+                double dx = x0 - Xr[nb];
+                double dy = x1 - Xr[NMP + nb];
+                double dz = x2 - Xr[2 * NMP + nb];
                 dx = valid ? dx : 1.0;
                 dy = valid ? dy : 0.0;
                 dz = valid ? dz : 0.0;
@@ -239,8 +249,8 @@ __global__ void __launch_bounds__(NMP, 1) lattice_kernel(LatArgs A) {
                 const double rest = r0 + (SA[vox] * r0) * D[vox];
                 const double inv_len = rcp_rn_fast(len);
                 const double nx = dx * inv_len, ny = dy * inv_len, nz = dz * inv_len;
-                const double rel = (Xr[3 * NMP + nb] - v0) * nx + (Xr[4 * NMP + nb] - v1) * ny +
-                                   (Xr[5 * NMP + nb] - v2) * nz;
+                const double rel = (v0 - Xr[3 * NMP + nb]) * nx + (v1 - Xr[4 * NMP + nb]) * ny +
+                                   (v2 - Xr[5 * NMP + nb]) * nz;
                 const double mag = pk[d] * (len - rest) + PC[d * NMP + a] * rel;
                 ofx[q] = mag * nx;
                 ofy[q] = mag * ny;
@@ -248,9 +258,12 @@ __global__ void __launch_bounds__(NMP, 1) lattice_kernel(LatArgs A) {
             }
 #pragma unroll
             for (int q = 0; q < kChunk; ++q) {
-                const int d = c0 + q;
-                if (d >= 13) break;
-                if ((fmask >> d) & 1u) {
+                const int d = c0 - q;
+                if (d < 0) break;
+                if ((bmask >> d) & 1u) {
+                    sx -= ofx[q];  // fx += (-1)*F == fx - F exactly
+                    sy -= ofy[q];
+                    sz -= ofz[q];
                     F[(3 * d) * NMP + a] = ofx[q];
                     F[(3 * d + 1) * NMP + a] = ofy[q];
                     F[(3 * d + 2) * NMP + a] = ofz[q];
@@ -266,22 +279,16 @@ __global__ void __launch_bounds__(NMP, 1) lattice_kernel(LatArgs A) {
         // ---- phase 2: ascending spring index = backward d = 12..0, forward d = 0..12
         int bad = 0;
         if (live) {
-            double fx = 0.0, fy = 0.0, fz = 0.0;
-#pragma unroll
-            for (int d = 12; d >= 0; --d) {
-                if (bmask & (1u << d)) {
-                    const int nb = static_cast<int>((bnb[d >> 1] >> (16 * (d & 1))) & 0xFFFFu);
-                    fx -= F[(3 * d) * NMP + nb];
-                    fy -= F[(3 * d + 1) * NMP + nb];
-                    fz -= F[(3 * d + 2) * NMP + nb];
-                }
-            }
+            // continue the ordered sum with the forward springs d = 0..12
+            // (ascending j), whose forces their higher endpoints stored
+            double fx = sx, fy = sy, fz = sz;
 #pragma unroll
             for (int d = 0; d < 13; ++d) {
                 if (fmask & (1u << d)) {
-                    fx += F[(3 * d) * NMP + a];
-                    fy += F[(3 * d + 1) * NMP + a];
-                    fz += F[(3 * d + 2) * NMP + a];
+                    const int nb = static_cast<int>((fnb[d >> 1] >> (16 * (d & 1))) & 0xFFFFu);
+                    fx += F[(3 * d) * NMP + nb];
+                    fy += F[(3 * d + 1) * NMP + nb];
+                    fz += F[(3 * d + 2) * NMP + nb];
                 }
             }
             if (en_grav) fz -= mg;
