@@ -136,12 +136,20 @@ __global__ void __launch_bounds__(NMP, 1) lattice_kernel(LatArgs A) {
 #pragma unroll
     for (int d = 0; d < 13; ++d) {
         pk[d] = 0.0;
-        pnb[d] = static_cast<uint32_t>(a) | (static_cast<uint32_t>(A.ncell) << 16);
+        pnb[d] = static_cast<uint32_t>(NMP - 1) | (static_cast<uint32_t>(A.ncell) << 16);  // ghost
         PR[d * NMP + a] = 1.0;
         PC[d * NMP + a] = 0.0;
     }
 #pragma unroll
     for (int q = 0; q < 7; ++q) fnb[q] = 0u;
+    if (a == NMP - 1) {  // ghost mass: far from every real mass, at rest; missing
+        X[a] = 1e3;      // springs point at it so every slot runs the same
+        X[NMP + a] = 1e3;  // branch-free code on the sqrt/div fast paths
+        X[2 * NMP + a] = 1e3;
+        X[3 * NMP + a] = 0.0;
+        X[4 * NMP + a] = 0.0;
+        X[5 * NMP + a] = 0.0;
+    }
     if (live) {
         x0 = b.pos[mo + a];
         x1 = b.pos[b.M + mo + a];
@@ -239,9 +247,6 @@ __global__ void __launch_bounds__(NMP, 1) lattice_kernel(LatArgs A) {
                 double dx = x0 - Xr[nb];
                 double dy = x1 - Xr[NMP + nb];
                 double dz = x2 - Xr[2 * NMP + nb];
-                dx = valid ? dx : 1.0;
-                dy = valid ? dy : 0.0;
-                dz = valid ? dz : 0.0;
                 const double len2 = dx * dx + dy * dy + dz * dz;
                 const double len = sqrt_rn_fast(len2);  // == sqrt(len2) on every used step (vx_internal.cuh)
                 zero_len |= (valid && len2 < A.zero_len2) ? 1 : 0;  // <=> sqrt(len2) < kZeroLengthEps
@@ -372,11 +377,12 @@ __global__ void __launch_bounds__(NMP, 1) lattice_kernel(LatArgs A) {
     }
 }
 
-constexpr int kNmpChoices[] = {64, 128, 160, 224, 256, 352, 384, 512};
+// NMP > max masses: slot NMP-1 is the ghost mass
+constexpr int kNmpChoices[] = {64, 128, 160, 224, 256, 352, 384, 512, 544};
 
 int pick_nmp(int nm_cap) {
     for (int c : kNmpChoices)
-        if (nm_cap <= c) return c;
+        if (nm_cap < c) return c;
     return -1;
 }
 
@@ -437,7 +443,8 @@ vx_status integrate_lattice(vx_ctx* ctx, vx_batch* b, const vx_sim* sim, int64_t
         case 256: return launch(lattice_kernel<256>, 256);
         case 352: return launch(lattice_kernel<352>, 352);
         case 384: return launch(lattice_kernel<384>, 384);
-        default: return launch(lattice_kernel<512>, 512);
+        case 512: return launch(lattice_kernel<512>, 512);
+        default: return launch(lattice_kernel<544>, 544);
     }
 }
 
