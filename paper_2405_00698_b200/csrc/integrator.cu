@@ -18,6 +18,8 @@
 //    come from a glibc-computed table, so on identical inputs the trajectory
 //    is BIT-IDENTICAL to the reference CPU integrator.
 #include <cmath>
+#include <cstdlib>
+#include <string>
 
 #include "vx_internal.cuh"
 
@@ -313,7 +315,11 @@ vx_status integrate(vx_ctx* ctx, vx_batch* b, const vx_sim* sim, int64_t k0, int
     if (grid <= 0) return VX_OK;
     VX_TRY(ensure_drive(ctx, sim->actuation_frequency, sim->dt, k0, n_steps > 0 ? n_steps : 1));
 
-    if (!d_robot_list && !d_summary_slot && lattice_applicable(ctx, b)) {
+    static const char* force = std::getenv("VX_INTEGRATOR");  // "generic" forces this file's kernel
+    const bool generic = force && std::string(force) == "generic";
+    const bool lat = !generic && !d_robot_list && !d_summary_slot && lattice_applicable(ctx, b);
+    const bool strm = !generic && !lat && !d_robot_list && !d_summary_slot && stream_applicable(ctx, b);
+    if (lat || strm) {
         const SimParams sp{sim->gravity, sim->dt, sim->enable_gravity, sim->enable_contact, b->plane.k,
                            b->plane.mu_static, b->plane.mu_kinetic};
         std::pair<cudaEvent_t, cudaEvent_t> ev{nullptr, nullptr};
@@ -327,7 +333,11 @@ vx_status integrate(vx_ctx* ctx, vx_batch* b, const vx_sim* sim, int64_t k0, int
             }
             VX_CUDA(cudaEventRecord(ev.first, ctx->stream));
         }
-        VX_TRY(integrate_lattice(ctx, b, sim, n_steps, write_back, d_summaries, sp));
+        if (lat) {
+            VX_TRY(integrate_lattice(ctx, b, sim, n_steps, write_back, d_summaries, sp));
+        } else {
+            VX_TRY(integrate_stream(ctx, b, n_steps, write_back, d_summaries, sp, zero_len2_threshold()));
+        }
         if (ctx->timing) {
             VX_CUDA(cudaEventRecord(ev.second, ctx->stream));
             ctx->pending.push_back(ev);

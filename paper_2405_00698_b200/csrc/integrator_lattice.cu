@@ -390,6 +390,15 @@ size_t lattice_smem(int nmp, int ncell) { return (73ull * nmp + 4ull * (ncell + 
 
 }  // namespace
 
+// sqrt is monotone and correctly rounded (host and device alike), so
+// len < eps  <=>  len^2 < T with T the smallest double whose sqrt >= eps
+double zero_len2_threshold() {
+    double t = kZeroLengthEps * kZeroLengthEps;
+    while (std::sqrt(t) >= kZeroLengthEps) t = std::nextafter(t, 0.0);
+    while (std::sqrt(t) < kZeroLengthEps) t = std::nextafter(t, 1.0);
+    return t;
+}
+
 // false when the batch is not a device-built lattice batch or is too large;
 // the caller then uses the generic kernel (integrator.cu).
 bool lattice_applicable(vx_ctx* ctx, vx_batch* b) {
@@ -420,13 +429,7 @@ vx_status integrate_lattice(vx_ctx* ctx, vx_batch* b, const vx_sim* sim, int64_t
     A.vh = b->lh + 1;
     A.nv = (b->lw + 1) * (b->lh + 1) * (b->ld + 1);
     A.ncell = b->lw * b->lh * b->ld;
-    {   // sqrt is monotone and correctly rounded (host and device alike), so
-        // len < eps  <=>  len^2 < T with T the smallest double whose sqrt >= eps
-        double t = kZeroLengthEps * kZeroLengthEps;
-        while (std::sqrt(t) >= kZeroLengthEps) t = std::nextafter(t, 0.0);
-        while (std::sqrt(t) < kZeroLengthEps) t = std::nextafter(t, 1.0);
-        A.zero_len2 = t;
-    }
+    A.zero_len2 = zero_len2_threshold();
     const size_t smem = lattice_smem(A.nmp, A.ncell);
     auto launch = [&](auto kernel, int threads) -> vx_status {
         VX_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
