@@ -394,6 +394,8 @@ vx_status build_batch_into(vx_ctx* ctx, vx_batch* b, int n, int w, int h, int d,
     A.vkey = b->vkey.p;
     A.act_vox = b->act_vox.p;
     b->lattice = true;
+    b->uniform_mass = table->mass_per_vertex;
+    b->uniform_zeta = table->damping_ratio;
     b->lw = w;
     b->lh = h;
     b->ld = d;

@@ -31,7 +31,7 @@ struct StreamLayout {
     int nmp, mpt, threads;
     size_t per_robot;  // bytes
     // offsets (bytes) inside a robot's scratch
-    size_t k, r0, c, ar, f, s, mc, x, pnb, fnb, mask, cph, sph;
+    size_t k, r0, f, s, mc, x, pnb, fnb, mask, cph, sph, sa;
 };
 
 StreamLayout stream_layout(int nm_cap, int ncell) {
@@ -48,8 +48,6 @@ StreamLayout stream_layout(int nm_cap, int ncell) {
     const size_t n = static_cast<size_t>(L.nmp);
     L.k = take(13 * n * 8);
     L.r0 = take(13 * n * 8);
-    L.c = take(13 * n * 8);
-    L.ar = take(13 * n * 8);
     L.f = take(39 * n * 8);
     L.s = take(3 * n * 8);
     L.mc = take(3 * n * 8);
@@ -59,6 +57,7 @@ StreamLayout stream_layout(int nm_cap, int ncell) {
     L.mask = take(n * 4);
     L.cph = take((ncell + 1) * 8ull);
     L.sph = take((ncell + 1) * 8ull);
+    L.sa = take((ncell + 1) * 8ull);
     L.per_robot = o;
     return L;
 }
@@ -67,6 +66,8 @@ struct StreamArgs {
     BatchView b;
     const int32_t* vkey;
     const int16_t* act_vox;
+    const double* sign;
+    const double* amp;
     const double2* drive;
     SimParams sp;
     int64_t n_steps;
@@ -77,6 +78,7 @@ struct StreamArgs {
     int vw, vh, ncell;
     double zero_len2;
     bool x_in_smem;
+    double zeta2, mu;  // damping: c = (zeta*2) * sqrt(k * mu); built robots have uniform masses
 };
 
 template <typename T>
@@ -93,11 +95,10 @@ __global__ void __launch_bounds__(1024) stream_prep_kernel(StreamArgs A) {
     unsigned char* base = A.scratch + static_cast<size_t>(r) * L.per_robot;
     double* K = at<double>(base, L.k);
     double* R0 = at<double>(base, L.r0);
-    double* C = at<double>(base, L.c);
-    double* AR = at<double>(base, L.ar);
     double* MC = at<double>(base, L.mc);
     double* XG = at<double>(base, L.x);
     double* F = at<double>(base, L.f);
+    double* SAG = at<double>(base, L.sa);
     uint32_t* PNB = at<uint32_t>(base, L.pnb);
     uint32_t* FNB = at<uint32_t>(base, L.fnb);
     uint32_t* MASK = at<uint32_t>(base, L.mask);
@@ -109,6 +110,7 @@ __global__ void __launch_bounds__(1024) stream_prep_kernel(StreamArgs A) {
     for (int v = threadIdx.x; v <= A.ncell; v += blockDim.x) {
         CPH[v] = 1.0;  // dummy passive voxel: D = sin(wt), amp_rest = 0
         SPH[v] = 0.0;
+        SAG[v] = 0.0;
     }
     __syncthreads();
     for (int s = threadIdx.x; s < ns; s += blockDim.x) {
@@ -116,14 +118,13 @@ __global__ void __launch_bounds__(1024) stream_prep_kernel(StreamArgs A) {
         if (v >= 0) {
             CPH[v] = b.cosph[so + s];
             SPH[v] = b.sinph[so + s];
+            SAG[v] = A.sign[so + s] * A.amp[so + s];  // sign * amplitude (physics.hpp:153)
         }
     }
     for (int a = threadIdx.x; a < NMP; a += blockDim.x) {
         for (int d = 0; d < 13; ++d) {
-            K[d * NMP + a] = 0.0;
+            K[d * NMP + a] = 1.0;  // missing spring: any normal value (its result is discarded)
             R0[d * NMP + a] = 1.0;
-            C[d * NMP + a] = 0.0;
-            AR[d * NMP + a] = 0.0;
             PNB[d * NMP + a] = static_cast<uint32_t>(GH) | (static_cast<uint32_t>(A.ncell) << 14);
         }
         for (int q = 0; q < 7; ++q) FNB[q * NMP + a] = 0u;
@@ -160,8 +161,6 @@ __global__ void __launch_bounds__(1024) stream_prep_kernel(StreamArgs A) {
                     bmask |= 1u << d;
                     K[d * NMP + a] = b.k[so + s];
                     R0[d * NMP + a] = b.rest0[so + s];
-                    C[d * NMP + a] = b.c[so + s];
-                    AR[d * NMP + a] = b.amp_rest[so + s];  // (sign*amplitude)*rest0, 0 when passive
                     const int av = A.act_vox[so + s];
                     PNB[d * NMP + a] = static_cast<uint32_t>(other) |
                                        (static_cast<uint32_t>(av >= 0 ? av : A.ncell) << 14);
@@ -185,9 +184,8 @@ __global__ void __launch_bounds__(512, 1) stream_kernel(StreamArgs A) {
     unsigned char* base = A.scratch + static_cast<size_t>(r) * L.per_robot;
     const double* K = at<double>(base, L.k);
     const double* R0 = at<double>(base, L.r0);
-    const double* C = at<double>(base, L.c);
-    const double* AR = at<double>(base, L.ar);
     const double* MC = at<double>(base, L.mc);
+    const double* SAG = at<double>(base, L.sa);
     double* F = at<double>(base, L.f);
     double* S = at<double>(base, L.s);
     double* XG = at<double>(base, L.x);
@@ -201,8 +199,9 @@ __global__ void __launch_bounds__(512, 1) stream_kernel(StreamArgs A) {
     vx_summary* out = A.out ? A.out + r : nullptr;
 
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    double* D = reinterpret_cast<double*>(smem_raw);  // [ncell + 1]
-    double* X = kXSmem ? D + A.ncell + 1 : XG;         // [6][NMP]
+    double* D = reinterpret_cast<double*>(smem_raw);  // [ncell + 1] drive per voxel
+    double* SA = D + A.ncell + 1;                      // [ncell + 1] sign*amplitude per voxel
+    double* X = kXSmem ? SA + A.ncell + 1 : XG;        // [6][NMP]
     __shared__ double s_maxsq[32];
     __shared__ double s_com[3];
 
@@ -221,7 +220,10 @@ __global__ void __launch_bounds__(512, 1) stream_kernel(StreamArgs A) {
         for (int q = t; q < 6 * NMP; q += T) X[q] = XG[q];
     {
         const double2 drv = __ldg(A.drive);
-        for (int v = t; v <= A.ncell; v += T) D[v] = drv.x * CPH[v] + drv.y * SPH[v];
+        for (int v = t; v <= A.ncell; v += T) {
+            D[v] = drv.x * CPH[v] + drv.y * SPH[v];
+            SA[v] = SAG[v];
+        }
     }
     __syncthreads();
     // center_of_mass (physics.hpp:266-278), sequential in mass order
@@ -278,12 +280,18 @@ __global__ void __launch_bounds__(512, 1) stream_kernel(StreamArgs A) {
                     const double len2 = dx * dx + dy * dy + dz * dz;
                     const double len = sqrt_rn_fast(len2);
                     zero_len |= (valid && len2 < A.zero_len2) ? 1 : 0;
-                    const double rest = R0[d * NMP + a] + AR[d * NMP + a] * D[vox];
+                    // amp_rest = (sign*amplitude)*rest0 (physics.hpp:153); passive -> 0
+                    const double r0 = R0[d * NMP + a];
+                    const double rest = r0 + (SA[vox] * r0) * D[vox];
                     const double inv_len = rcp_rn_fast(len);
                     const double nx = dx * inv_len, ny = dy * inv_len, nz = dz * inv_len;
                     const double rel = (v0 - X[3 * NMP + nb]) * nx + (v1 - X[4 * NMP + nb]) * ny +
                                        (v2 - X[5 * NMP + nb]) * nz;
-                    const double mag = K[d * NMP + a] * (len - rest) + C[d * NMP + a] * rel;
+                    // damping_coefficient (physics.hpp:66-71) recomputed: FP64 is idle in this
+                    // bandwidth-bound kernel, bytes are not (uniform masses: mu per robot)
+                    const double kk = K[d * NMP + a];
+                    const double cc = A.zeta2 * sqrt_rn_fast(kk * A.mu);
+                    const double mag = kk * (len - rest) + cc * rel;
                     ofx[q] = mag * nx;
                     ofy[q] = mag * ny;
                     ofz[q] = mag * nz;
@@ -417,11 +425,11 @@ __global__ void __launch_bounds__(512, 1) stream_kernel(StreamArgs A) {
 }  // namespace
 
 bool stream_applicable(vx_ctx* ctx, vx_batch* b) {
-    if (!b->lattice || !b->vkey.p || !b->act_vox.p) return false;
+    if (!b->lattice || !b->vkey.p || !b->act_vox.p || !(b->uniform_mass > 0.0)) return false;
     const int ncell = b->lw * b->lh * b->ld;
     if (ncell + 1 >= (1 << 18)) return false;  // voxel id packed in 18 bits
     if (b->nm_max + 1 > (1 << 14)) return false;  // neighbour packed in 14 bits
-    return (ncell + 1) * sizeof(double) + 1024 <= ctx->smem_optin;
+    return 2ull * (ncell + 1) * sizeof(double) + 1024 <= ctx->smem_optin;
 }
 
 vx_status integrate_stream(vx_ctx* ctx, vx_batch* b, int64_t n_steps, bool write_back, vx_summary* d_summaries,
@@ -430,6 +438,8 @@ vx_status integrate_stream(vx_ctx* ctx, vx_batch* b, int64_t n_steps, bool write
     A.b = view_of(b);
     A.vkey = b->vkey.p;
     A.act_vox = b->act_vox.p;
+    A.sign = b->sign.p;
+    A.amp = b->amp.p;
     A.drive = ctx->drive.p;
     A.sp = sp;
     A.n_steps = n_steps;
@@ -439,10 +449,12 @@ vx_status integrate_stream(vx_ctx* ctx, vx_batch* b, int64_t n_steps, bool write
     A.vh = b->lh + 1;
     A.ncell = b->lw * b->lh * b->ld;
     A.zero_len2 = zero_len2;
+    A.zeta2 = b->uniform_zeta * 2.0;
+    A.mu = b->uniform_mass * b->uniform_mass / (b->uniform_mass + b->uniform_mass);
     A.L = stream_layout(b->nm_max, A.ncell);
     VX_TRY(ctx->stream_scratch.alloc(A.L.per_robot * static_cast<size_t>(b->n)));
     A.scratch = ctx->stream_scratch.p;
-    const size_t smem_d = (A.ncell + 1) * sizeof(double);
+    const size_t smem_d = 2ull * (A.ncell + 1) * sizeof(double);
     const size_t smem_x = 6ull * A.L.nmp * sizeof(double);
     A.x_in_smem = smem_d + smem_x + 2048 <= ctx->smem_optin;
     stream_prep_kernel<<<b->n, 1024, 0, ctx->stream>>>(A);
