@@ -274,6 +274,27 @@ vx_status vx_evo_set_params(vx_evo* e, const vx_hyper* h); /* clamped like the a
 int32_t vx_evo_generation_index(vx_evo* e);
 /* best_fitness / best_genome (evolution.hpp:246-249); returns 1 if set. */
 int32_t vx_evo_best(vx_evo* e, double* best_fitness, double* best_params);
+/* The same plus the best genome's frozen B matrix (3m doubles): the
+ * best_genome of a checkpoint (serialize.hpp:227-231). */
+int32_t vx_evo_best_genome(vx_evo* e, double* best_fitness, double* best_params, double* best_bmat);
+/* Resume support (evolution_state_from_json, serialize.hpp:235-262): set the
+ * generation counter and best_fitness / best_genome (params and B both NULL =
+ * no best genome yet).  Together with vx_evo_set_population (grids NULL),
+ * vx_evo_set_params and vx_evo_set_rng_state this restores a checkpoint so
+ * that the resumed run is identical to an uninterrupted one
+ * (test_serialize.cpp:105-131). */
+vx_status vx_evo_set_progress(vx_evo* e, int32_t generation, double best_fitness, const double* best_params,
+                              const double* best_bmat);
+
+/* ------------------------------------------------------- file formats --- */
+/* Host only.  The JSON text of n doubles, separated by `sep`, exactly as the
+ * reference's checkpoints print them (nlohmann::json dump(): Grisu2 digits,
+ * "1.0", "1e-05"), so checkpoint checksums (serialize.hpp:264-292) and
+ * curves.csv (serialize.hpp:321-343) are byte-identical.  Returns the text
+ * length (written NUL-terminated into out when cap allows), -1 on bad args. */
+int64_t vx_format_doubles(const double* v, int64_t n, char sep, char* out, int64_t cap);
+/* Host only.  FNV-1a 64 of n bytes: the checkpoint checksum (serialize.hpp:23-28). */
+uint64_t vx_fnv1a64(const char* data, int64_t n);
 
 /* ------------------------------------------------------- measurement ---- */
 /* Live CUDA-event timing of every integrator launch on the context stream

@@ -428,6 +428,66 @@ def have_reference() -> bool:
     return os.path.exists(REF_SO)
 
 
+REF_IO_SO = os.path.join(HERE, "_ref", "libvoxevo_ref_io.so")
+
+
+class RefIO:
+    """The reference's serialize.hpp (checkpoints, curves) and its JSON
+    library's number printing, behind oracle/ref_io_shim.cpp."""
+
+    def __init__(self, path: str = REF_IO_SO):
+        lib = C.CDLL(path)
+        i64, vp, cp = C.c_int64, C.c_void_p, C.c_char_p
+        lib.ref_io_last_error.restype = cp
+        lib.ref_io_dump_doubles.restype = i64
+        lib.ref_io_dump_doubles.argtypes = [vp, i64, cp, i64]
+        lib.ref_io_fnv_hex.restype = i64
+        lib.ref_io_fnv_hex.argtypes = [cp, cp, i64]
+        lib.ref_io_run_and_save.restype = C.c_int
+        lib.ref_io_run_and_save.argtypes = [cp, C.c_int, cp]
+        lib.ref_io_resume.restype = C.c_int
+        lib.ref_io_resume.argtypes = [cp, C.c_int, cp]
+        lib.ref_io_curves_csv.restype = i64
+        lib.ref_io_curves_csv.argtypes = [cp, cp, i64]
+        self.lib = lib
+
+    def _text(self, fn, *args) -> str:
+        n = fn(*args, None, 0)
+        if n < 0:
+            raise RuntimeError(self.lib.ref_io_last_error().decode())
+        buf = C.create_string_buffer(n + 1)
+        fn(*args, buf, n + 1)
+        return buf.raw[:n].decode()
+
+    def dump_doubles(self, v: np.ndarray) -> list:
+        v = np.ascontiguousarray(v, np.float64)
+        return self._text(self.lib.ref_io_dump_doubles, v.ctypes.data, v.size)[1:-1].split(",")
+
+    def fnv_hex(self, s: str) -> str:
+        return self._text(self.lib.ref_io_fnv_hex, s.encode())
+
+    def run_and_save(self, config_json: str, gens: int, path: str):
+        if self.lib.ref_io_run_and_save(config_json.encode(), gens, path.encode()) != 0:
+            raise RuntimeError(self.lib.ref_io_last_error().decode())
+
+    def resume(self, in_path: str, gens: int, out_path: str):
+        if self.lib.ref_io_resume(in_path.encode(), gens, out_path.encode()) != 0:
+            raise RuntimeError(self.lib.ref_io_last_error().decode())
+
+    def curves_csv(self, path: str) -> str:
+        return self._text(self.lib.ref_io_curves_csv, path.encode())
+
+
+def have_reference_io() -> bool:
+    return os.path.exists(REF_IO_SO)
+
+
+def reference_io() -> RefIO:
+    if "io" not in _cache:
+        _cache["io"] = RefIO()
+    return _cache["io"]
+
+
 # --------------------------------------------------------------------------
 # Hand-built systems used by the reference's own physics tests
 # (test_physics.cpp:13-27, acceptance_main.cpp:77-92).

@@ -263,11 +263,15 @@ def _declare(lib):
         "vx_evo_set_params": (i32, [vp, P(HyperParams)]),
         "vx_evo_generation_index": (i32, [vp]),
         "vx_evo_best": (i32, [vp, P(dbl), vp]),
+        "vx_evo_best_genome": (i32, [vp, P(dbl), vp, vp]),
+        "vx_evo_set_progress": (i32, [vp, i32, dbl, vp, vp]),
         "vx_run_bench": (i32, [vp, i32, i64, i32, dbl, vp]),
         "vx_timing_enable": (i32, [vp, i32]),
         "vx_integrator_timing": (i32, [vp, P(dbl), P(i64), i32]),
         "vx_fp64_peak": (i32, [vp, P(dbl)]),
         "vx_fastmath_check": (i32, [vp, i64, u64, vp]),
+        "vx_format_doubles": (i64, [vp, i64, C.c_char, C.c_char_p, i64]),
+        "vx_fnv1a64": (u64, [C.c_char_p, i64]),
     }
     for name, (res, args) in sigs.items():
         fn = getattr(lib, name)
@@ -632,6 +636,27 @@ class EvolutionState:
         has = _lib().vx_evo_best(self.h, C.byref(bf), _ptr(bp))
         return float(bf.value), (bp if has else None)
 
+    def _best_bmat(self):
+        bf = C.c_double()
+        bp = np.zeros(self.np)
+        bb = np.zeros(3 * self.config.arch.m)
+        has = _lib().vx_evo_best_genome(self.h, C.byref(bf), _ptr(bp), _ptr(bb))
+        return bb if has else None
+
+    def set_progress(self, generation: int, best_fitness: float, best=None):
+        """Resume support: generation counter and best_fitness / best_genome
+        (``best`` = (params, bmat) or None)."""
+        if best is None:
+            _check(_lib().vx_evo_set_progress(self.h, int(generation), float(best_fitness), None, None),
+                   "set_progress")
+        else:
+            bp = np.ascontiguousarray(best[0], np.float64)
+            bb = np.ascontiguousarray(best[1], np.float64)
+            if bp.size != self.np or bb.size != 3 * self.config.arch.m:
+                raise ValueError("best genome shape does not match the architecture")
+            _check(_lib().vx_evo_set_progress(self.h, int(generation), float(best_fitness), _ptr(bp), _ptr(bb)),
+                   "set_progress")
+
     def rng_state(self) -> str:
         n = _lib().vx_evo_rng_state(self.h, None, 0)
         buf = C.create_string_buffer(int(n) + 1)
@@ -715,3 +740,8 @@ def report_dict(r: GenerationReport) -> dict:
     return dict(generation=r.generation, evaluations=r.evaluations, best=r.best, mean=r.mean, stddev=r.stddev,
                 diversity=r.diversity, wall_time=r.wall_time, spring_updates=int(r.spring_updates),
                 params=r.params.as_array())
+
+
+# config files and checkpoints (config.hpp / serialize.hpp formats)
+from .serialize import (CheckpointError, ConfigError, RunConfig, curves_csv, load_genome, load_run,  # noqa: E402
+                        load_run_config, run_config_from_json, save_genome, save_run, write_curves_csv)

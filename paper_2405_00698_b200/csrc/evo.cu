@@ -88,7 +88,7 @@ struct vx_evo {
     int generation = 0;
     double best_fitness = 0.0;
     bool has_best = false;
-    std::vector<double> best_genome;
+    std::vector<double> best_genome, best_bmat;
     // begin/finish
     bool begun = false;
     std::vector<int32_t> todo;
@@ -354,6 +354,9 @@ vx_status vx_evo_finish(vx_evo* e, vx_report* rep) {
         e->best_genome.resize(e->np);
         VX_CUDA(cudaMemcpy(e->best_genome.data(), e->prm[c].p + static_cast<size_t>(top) * e->np,
                            e->np * sizeof(double), cudaMemcpyDeviceToHost));
+        e->best_bmat.resize(e->nb);
+        VX_CUDA(cudaMemcpy(e->best_bmat.data(), e->bm[c].p + static_cast<size_t>(top) * e->nb,
+                           e->nb * sizeof(double), cudaMemcpyDeviceToHost));
         e->has_best = true;
     }
     vx_report r{};
@@ -530,6 +533,29 @@ int32_t vx_evo_best(vx_evo* e, double* best_fitness, double* best_params) {
     if (!e->has_best) return 0;
     if (best_params) std::copy(e->best_genome.begin(), e->best_genome.end(), best_params);
     return 1;
+}
+
+int32_t vx_evo_best_genome(vx_evo* e, double* best_fitness, double* best_params, double* best_bmat) {
+    const int32_t has = vx_evo_best(e, best_fitness, best_params);
+    if (has && best_bmat) std::copy(e->best_bmat.begin(), e->best_bmat.end(), best_bmat);
+    return has;
+}
+
+vx_status vx_evo_set_progress(vx_evo* e, int32_t generation, double best_fitness, const double* best_params,
+                              const double* best_bmat) {
+    if (!e || generation < 0 || (best_params == nullptr) != (best_bmat == nullptr)) return VX_EINVAL;
+    if (e->begun) return (set_error("progress change mid-generation"), VX_ESTATE);
+    e->generation = generation;
+    e->best_fitness = best_fitness;
+    e->has_best = best_params != nullptr;
+    if (best_params) {
+        e->best_genome.assign(best_params, best_params + e->np);
+        e->best_bmat.assign(best_bmat, best_bmat + e->nb);
+    } else {
+        e->best_genome.clear();
+        e->best_bmat.clear();
+    }
+    return VX_OK;
 }
 
 }  // extern "C"
