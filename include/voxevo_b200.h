@@ -297,6 +297,12 @@ int64_t vx_format_doubles(const double* v, int64_t n, char sep, char* out, int64
 uint64_t vx_fnv1a64(const char* data, int64_t n);
 
 /* ------------------------------------------------------- measurement ---- */
+/* Which integrator kernel the last simulate/step/evaluate launch used:
+ * generic (any uploaded system), lattice (one CTA per robot, <= 351 masses),
+ * cluster (one thread-block cluster per robot, 7^3..10^3 grids), stream
+ * (per-slot arrays through L2/HBM, larger grids).  -1 before any launch. */
+enum { VX_KERNEL_GENERIC = 0, VX_KERNEL_LATTICE = 1, VX_KERNEL_CLUSTER = 2, VX_KERNEL_STREAM = 3 };
+int32_t vx_last_integrator(vx_ctx* ctx);
 /* Live CUDA-event timing of every integrator launch on the context stream
  * (roofline reporting): enable, run, then read (and optionally reset) the
  * summed device time and launch count. */

@@ -219,6 +219,7 @@ def _declare(lib):
         "vx_get_stream": (vp, [vp]),
         "vx_synchronize": (i32, [vp]),
         "vx_launch_count": (u64, [vp]),
+        "vx_last_integrator": (i32, [vp]),
         "vx_device_info": (i32, [vp, P(i32), P(i32), C.c_char_p, i32]),
         "vx_sample_genomes_dev": (i32, [vp, P(Arch), i32, vp, vp, vp]),
         "vx_decode_dev": (i32, [vp, P(Arch), i32, vp, vp, i32, i32, i32, vp, vp, vp]),
@@ -350,6 +351,12 @@ class Context:
     @property
     def launches(self) -> int:
         return int(_lib().vx_launch_count(self.h))
+
+    @property
+    def last_integrator(self) -> str:
+        """Kernel of the last integrator launch: generic | lattice | cluster | stream."""
+        k = int(_lib().vx_last_integrator(self.h))
+        return {0: "generic", 1: "lattice", 2: "cluster", 3: "stream"}.get(k, "none")
 
     def timing(self, on: bool = True):
         _check(_lib().vx_timing_enable(self.h, 1 if on else 0))

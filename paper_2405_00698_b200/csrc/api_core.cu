@@ -251,6 +251,7 @@ vx_status vx_synchronize(vx_ctx* ctx) {
     return VX_OK;
 }
 uint64_t vx_launch_count(vx_ctx* ctx) { return ctx ? ctx->launches : 0; }
+int32_t vx_last_integrator(vx_ctx* ctx) { return ctx ? ctx->last_integrator : -1; }
 vx_status vx_device_info(vx_ctx* ctx, int32_t* sm_count, int32_t* clock_khz, char* name, int32_t name_cap) {
     if (!ctx) return VX_EINVAL;
     if (sm_count) *sm_count = ctx->sm_count;

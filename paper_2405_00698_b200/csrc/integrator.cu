@@ -318,8 +318,9 @@ vx_status integrate(vx_ctx* ctx, vx_batch* b, const vx_sim* sim, int64_t k0, int
     static const char* force = std::getenv("VX_INTEGRATOR");  // "generic" forces this file's kernel
     const bool generic = force && std::string(force) == "generic";
     const bool lat = !generic && !d_robot_list && !d_summary_slot && lattice_applicable(ctx, b);
-    const bool strm = !generic && !lat && !d_robot_list && !d_summary_slot && stream_applicable(ctx, b);
-    if (lat || strm) {
+    const bool clus = !generic && !lat && !d_robot_list && !d_summary_slot && cluster_applicable(ctx, b);
+    const bool strm = !generic && !lat && !clus && !d_robot_list && !d_summary_slot && stream_applicable(ctx, b);
+    if (lat || clus || strm) {
         const SimParams sp{sim->gravity, sim->dt, sim->enable_gravity, sim->enable_contact, b->plane.k,
                            b->plane.mu_static, b->plane.mu_kinetic};
         std::pair<cudaEvent_t, cudaEvent_t> ev{nullptr, nullptr};
@@ -333,8 +334,11 @@ vx_status integrate(vx_ctx* ctx, vx_batch* b, const vx_sim* sim, int64_t k0, int
             }
             VX_CUDA(cudaEventRecord(ev.first, ctx->stream));
         }
+        ctx->last_integrator = lat ? VX_KERNEL_LATTICE : clus ? VX_KERNEL_CLUSTER : VX_KERNEL_STREAM;
         if (lat) {
             VX_TRY(integrate_lattice(ctx, b, sim, n_steps, write_back, d_summaries, sp));
+        } else if (clus) {
+            VX_TRY(integrate_cluster(ctx, b, n_steps, write_back, d_summaries, sp, zero_len2_threshold()));
         } else {
             VX_TRY(integrate_stream(ctx, b, n_steps, write_back, d_summaries, sp, zero_len2_threshold()));
         }
@@ -345,6 +349,7 @@ vx_status integrate(vx_ctx* ctx, vx_batch* b, const vx_sim* sim, int64_t k0, int
         return VX_OK;
     }
 
+    ctx->last_integrator = VX_KERNEL_GENERIC;
     KernelArgs A{};
     A.b = view_of(b);
     A.drive = ctx->drive.p;

@@ -1,0 +1,560 @@
+// integrator_cluster.cu — K7c: the on-chip lattice integrator for robots too
+// big for one SM (352 .. 1,404 masses: 7^3 .. 10^3 grids, the robots of
+// configs 3 and 4).
+//
+// Same algorithm and bit-exact results as integrator_lattice.cu (step()
+// physics.hpp:191-264, simulate() :287-311): the higher endpoint of every
+// lattice spring computes it in phase 1 for d = 12..0 (the head of the
+// reference's ascending-spring-index gather, accumulated in registers), then
+// phase 2 adds the forward terms d = 0..12 and integrates.  What changes is the
+// placement: ONE THREAD-BLOCK CLUSTER PER ROBOT.
+//
+//  * The robot's masses (z-major index order) are split into CL contiguous
+//    ranges of q masses, one per CTA of the cluster (CL = 2..4, q <= 351), one
+//    thread per mass, everything (state, force slots, rest lengths, damping,
+//    per-voxel drive) in that CTA's shared memory: nothing streams from HBM.
+//  * Lattice springs reach at most H = vw*vh + vw + 1 mass indices back, so a
+//    CTA needs the state of the previous CTA's last H masses: a HALO that the
+//    previous CTA pushes into this CTA's shared memory with st.shared::cluster
+//    right after it integrates them (phase 2).
+//  * Force slots are indexed by the LOWER endpoint, F[d][i]: the higher
+//    endpoint stores each force once, into its own CTA or — for the ~1.1k
+//    springs that cross a range boundary — straight into the previous CTA's
+//    shared memory (DSMEM stores, fire-and-forget, spread over phase 1).
+//    Phase 2 then reads only local, contiguous slots.
+//  * Two cluster barriers per step (barrier.cluster arrive.release /
+//    wait.acquire) replace the two __syncthreads of the one-SM kernel; the
+//    zero-length / divergence flags are broadcast to every CTA's flag word
+//    before the barrier (rare path), tagged with the step so no reset is
+//    needed.
+// Compiled with --fmad=false; all sums in reference order.
+#include <cmath>
+#include <cstdlib>
+#include <string>
+
+#include "vx_internal.cuh"
+
+namespace vx {
+namespace {
+
+constexpr int kNmp = 352;              // threads per CTA; owned masses <= kNmp - 1
+constexpr int kXS = 512;               // X row stride: [halo | own kNmp | ghost]
+constexpr int kH0 = kXS - kNmp - 1;    // own mass a lives at X index kH0 + a; halo below
+constexpr int kGhost = kXS - 1;        // far-away resting mass for missing springs
+constexpr int kVpt = 3;                // voxels per thread (drive table rows kept in registers)
+constexpr int kMaxCluster = 4;
+
+struct ClArgs {
+    BatchView b;
+    const int32_t* vkey;
+    const int16_t* act_vox;
+    const double* sign;
+    const double* amp;
+    const double2* drive;
+    SimParams sp;
+    int64_t n_steps;
+    int write_back;
+    vx_summary* out;
+    double* xfinal;  // [6][M] final state, read back by rank 0 for the centre of mass
+    int cl;          // CTAs per robot
+    int halo;        // H: max backward mass-index offset of a lattice spring
+    int vw, vh, ncell;
+    double zero_len2;
+};
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ uint32_t map_rank(uint32_t addr, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void st_remote(uint32_t addr, double v) {
+    asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(addr), "d"(v));
+}
+__device__ __forceinline__ void st_remote_u32(uint32_t addr, uint32_t v) {
+    asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(addr), "r"(v));
+}
+__device__ __forceinline__ void cluster_barrier() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+
+__global__ void __launch_bounds__(kNmp, 1) cluster_kernel(ClArgs A) {
+    const int cl = A.cl;
+    const uint32_t rank = cluster_rank();
+    const int r = blockIdx.x / cl;
+    const BatchView& b = A.b;
+    const int64_t mo = b.mass_off[r], so = b.spring_off[r];
+    const int nm = b.nmass[r];
+    const int a = threadIdx.x;
+    vx_summary* out = (A.out && rank == 0) ? A.out + r : nullptr;
+
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    double* X = reinterpret_cast<double*>(smem_raw);  // [6][kXS]  x y z vx vy vz
+    double* F = X + 6 * kXS;                           // [13*3][kNmp] force on i of spring (i, i+off_d)
+    double* PR = F + 39 * kNmp;                        // [13][kNmp] rest0 of backward slot (d, a)
+    double* PC = PR + 13 * kNmp;                       // [13][kNmp] damping coefficient of slot (d, a)
+    const int NT = A.ncell + 1;                        // voxel tables + dummy passive entry
+    double* D = PC + 13 * kNmp;                        // [NT] drive per voxel
+    double* SA = D + NT;                               // [NT] sign*amplitude (0 for the dummy)
+    __shared__ double s_maxsq[kNmp / 32];
+    __shared__ double s_cmax[kMaxCluster];
+    __shared__ uint32_t s_flag;
+
+    if (nm == 0) {  // uniform over the cluster: every CTA leaves, rank 0 reports
+        if (out && a == 0) {
+            for (int c = 0; c < 3; ++c) out->com_start[c] = out->com_end[c] = 0.0;
+            out->horizontal_displacement = 0.0;
+            out->max_speed = 0.0;
+            out->diverged = 0;
+            out->steps = 0;
+            out->spring_updates = 0;
+        }
+        return;
+    }
+
+    // ---------------------------------------------------------- ranges
+    const int H = A.halo;
+    int q = (nm + cl - 1) / cl;
+    if (q < H) q = H;  // a backward neighbour is never more than one CTA away
+    const int lo = static_cast<int>(rank) * q;
+    const int hi = min(nm, lo + q);
+    const int nown = max(0, hi - lo);
+    const bool live = a < nown;
+    const int g = lo + a;                                    // global mass index of this thread
+    const bool has_next = static_cast<int>(rank) + 1 < cl && lo + q < nm;
+    const bool push_halo = live && has_next && g >= lo + q - H;  // next CTA reads this mass's state
+    const bool warp_live = (a & ~31) < nown;
+
+    // ---------------------------------------------------------- prologue
+    // voxel tables: SA in place; sin/cos(phase) staged in the (still unused)
+    // force area, then kept in registers (kVpt voxels per thread)
+    double* SPH = F;
+    double* CPH = F + NT;
+    for (int v = a; v < NT; v += kNmp) {
+        SA[v] = 0.0;
+        SPH[v] = 0.0;
+        CPH[v] = 1.0;
+    }
+    if (a == 0) s_flag = 0u;
+    __syncthreads();
+    const int ns = b.nspring[r];
+    for (int s = a; s < ns; s += kNmp) {  // per-voxel actuation, identical for all its springs
+        const int v = A.act_vox[so + s];
+        if (v >= 0) {
+            SA[v] = A.sign[so + s] * A.amp[so + s];  // sign * amplitude (physics.hpp:153)
+            SPH[v] = b.sinph[so + s];
+            CPH[v] = b.cosph[so + s];
+        }
+    }
+    // state: own masses, the halo below them, the ghost
+    for (int li = kH0 - H + a; li < kH0; li += kNmp) {
+        const int gg = lo - kH0 + li;
+        if (gg >= 0) {
+            for (int c = 0; c < 3; ++c) {
+                X[c * kXS + li] = b.pos[c * b.M + mo + gg];
+                X[(3 + c) * kXS + li] = b.vel[c * b.M + mo + gg];
+            }
+        }
+    }
+    if (a == 0) {
+        X[kGhost] = 1e3;
+        X[kXS + kGhost] = 1e3;
+        X[2 * kXS + kGhost] = 1e3;
+        X[3 * kXS + kGhost] = 0.0;
+        X[4 * kXS + kGhost] = 0.0;
+        X[5 * kXS + kGhost] = 0.0;
+    }
+    double pk[13];
+    uint32_t pnb[13];  // X index of the lower neighbour | voxel << 9 (ncell = passive/missing)
+    unsigned fmask = 0u, bmask = 0u;
+    double mg = 0.0, imdt = 0.0, gdmp = 0.0;
+    double x0 = 0.0, x1 = 0.0, x2 = 0.0, v0 = 0.0, v1 = 0.0, v2 = 0.0;
+#pragma unroll
+    for (int d = 0; d < 13; ++d) {
+        pk[d] = 0.0;
+        pnb[d] = static_cast<uint32_t>(kGhost) | (static_cast<uint32_t>(A.ncell) << 9);
+        PR[d * kNmp + a] = 1.0;
+        PC[d * kNmp + a] = 0.0;
+    }
+    if (live) {
+        x0 = b.pos[mo + g];
+        x1 = b.pos[b.M + mo + g];
+        x2 = b.pos[2 * b.M + mo + g];
+        v0 = b.vel[mo + g];
+        v1 = b.vel[b.M + mo + g];
+        v2 = b.vel[2 * b.M + mo + g];
+        X[kH0 + a] = x0;
+        X[kXS + kH0 + a] = x1;
+        X[2 * kXS + kH0 + a] = x2;
+        X[3 * kXS + kH0 + a] = v0;
+        X[4 * kXS + kH0 + a] = v1;
+        X[5 * kXS + kH0 + a] = v2;
+        const double m = b.mass[mo + g];
+        mg = m * A.sp.gravity;  // physics.hpp:226
+        imdt = A.sp.dt / m;     // physics.hpp:249
+        gdmp = b.gdamp[mo + g];
+        const int ka = A.vkey[mo + g];
+        const int xa = ka % A.vw, ya = (ka / A.vw) % A.vh, za = ka / (A.vw * A.vh);
+        const int32_t* inc_off = b.inc_off + mo + r;
+        const uint32_t* inc = b.inc + 2 * so;
+        for (int e = inc_off[g]; e < inc_off[g + 1]; ++e) {
+            const uint32_t iv = inc[e];
+            const int s = static_cast<int>(iv >> 1);
+            const uint32_t ij = b.ij[so + s];
+            const int other = (iv & 1u) ? static_cast<int>(ij & 0xFFFFu) : static_cast<int>(ij >> 16);
+            const int kb = A.vkey[mo + other];
+            const int dx = kb % A.vw - xa, dy = (kb / A.vw) % A.vh - ya, dz = kb / (A.vw * A.vh) - za;
+            const int L = 9 * dz + 3 * dy + dx;  // forward iff L > 0; direction d = |L| - 1
+            const int dd = (L > 0 ? L : -L) - 1;
+#pragma unroll
+            for (int d = 0; d < 13; ++d) {
+                if (d == dd) {
+                    if (L < 0) {  // spring (other, g): g is its higher endpoint and computes it
+                        bmask |= 1u << d;
+                        pk[d] = b.k[so + s];
+                        PR[d * kNmp + a] = b.rest0[so + s];
+                        PC[d * kNmp + a] = b.c[so + s];
+                        const int av = A.act_vox[so + s];
+                        pnb[d] = static_cast<uint32_t>(other - lo + kH0) |
+                                 (static_cast<uint32_t>(av >= 0 ? av : A.ncell) << 9);
+                    } else {  // spring (g, other): its force arrives in F[d][a]
+                        fmask |= 1u << d;
+                    }
+                }
+            }
+        }
+    }
+    __syncthreads();
+    double vsin[kVpt], vcos[kVpt];
+    {
+        const double2 drv = __ldg(A.drive);
+#pragma unroll
+        for (int j = 0; j < kVpt; ++j) {
+            const int v = a + j * kNmp;
+            vsin[j] = v < NT ? SPH[v] : 0.0;
+            vcos[j] = v < NT ? CPH[v] : 1.0;
+            if (v < NT) D[v] = drv.x * vcos[j] + drv.y * vsin[j];
+        }
+    }
+    double com_start[3] = {0.0, 0.0, 0.0};
+    if (out && a == 0) {  // center_of_mass (physics.hpp:266-278) of the initial state, in mass order
+        double c0 = 0.0, c1 = 0.0, c2 = 0.0, total = 0.0;
+        for (int m = 0; m < nm; ++m) {
+            const double w = b.mass[mo + m];
+            c0 += w * b.pos[mo + m];
+            c1 += w * b.pos[b.M + mo + m];
+            c2 += w * b.pos[2 * b.M + mo + m];
+            total += w;
+        }
+        if (total > 0.0) {
+            c0 /= total;
+            c1 /= total;
+            c2 /= total;
+        }
+        com_start[0] = c0;
+        com_start[1] = c1;
+        com_start[2] = c2;
+    }
+    // DSMEM targets: the previous CTA's force slots, the next CTA's state rows,
+    // every CTA's flag word
+    const uint32_t f_prev = rank > 0 ? map_rank(smem_addr(F), rank - 1) : 0u;
+    const uint32_t x_next = has_next ? map_rank(smem_addr(X), rank + 1) : 0u;
+    const uint32_t flag_local = smem_addr(&s_flag);
+    cluster_barrier();  // every CTA initialised before any remote store
+
+    const double dt = A.sp.dt;
+    const double plane_k = A.sp.plane_k, mu_s = A.sp.mu_s, mu_k = A.sp.mu_k;
+    const bool en_grav = A.sp.en_grav, en_contact = A.sp.en_contact;
+    double max_sq = 0.0;
+    int64_t steps = 0, ok_phase1 = 0;
+    int diverged = 0;
+    auto raise_flag = [&](uint32_t tag) {  // rare: tell every CTA before the barrier
+        for (int c = 0; c < cl; ++c) st_remote_u32(map_rank(flag_local, static_cast<uint32_t>(c)), tag);
+    };
+    for (int64_t kstep = 0; kstep < A.n_steps; ++kstep) {
+        const uint32_t tag1 = static_cast<uint32_t>(2 * kstep + 1), tag2 = tag1 + 1u;
+        // ---- phase 1: the backward springs of mass g, d = 12..0 (see integrator_lattice.cu)
+        int zero_len = 0;
+        double sx = 0.0, sy = 0.0, sz = 0.0;
+        if (warp_live) {
+            const double* __restrict__ Xr = X;
+            constexpr int kChunk = 5;
+#pragma unroll
+            for (int c0 = 12; c0 >= 0; c0 -= kChunk) {
+                double ofx[kChunk], ofy[kChunk], ofz[kChunk];
+#pragma unroll
+                for (int qq = 0; qq < kChunk; ++qq) {
+                    const int d = c0 - qq;
+                    if (d < 0) break;
+                    const bool valid = (bmask >> d) & 1u;
+                    const int nb = static_cast<int>(pnb[d] & 0x1FFu);
+                    const int vox = static_cast<int>(pnb[d] >> 9);
+                    // spring_force_on_i with i = nb, j = g (physics.hpp:55-64, 201-212)
+                    double dx = x0 - Xr[nb];
+                    double dy = x1 - Xr[kXS + nb];
+                    double dz = x2 - Xr[2 * kXS + nb];
+                    const double len2 = dx * dx + dy * dy + dz * dz;
+                    const double len = sqrt_rn_fast(len2);
+                    zero_len |= (valid && len2 < A.zero_len2) ? 1 : 0;
+                    const double r0 = PR[d * kNmp + a];
+                    const double rest = r0 + (SA[vox] * r0) * D[vox];
+                    const double inv_len = rcp_rn_fast(len);
+                    const double nx = dx * inv_len, ny = dy * inv_len, nz = dz * inv_len;
+                    const double rel = (v0 - Xr[3 * kXS + nb]) * nx + (v1 - Xr[4 * kXS + nb]) * ny +
+                                       (v2 - Xr[5 * kXS + nb]) * nz;
+                    const double mag = pk[d] * (len - rest) + PC[d * kNmp + a] * rel;
+                    ofx[qq] = mag * nx;
+                    ofy[qq] = mag * ny;
+                    ofz[qq] = mag * nz;
+                }
+#pragma unroll
+                for (int qq = 0; qq < kChunk; ++qq) {
+                    const int d = c0 - qq;
+                    if (d < 0) break;
+                    if ((bmask >> d) & 1u) {
+                        sx -= ofx[qq];  // fx += (-1)*F == fx - F exactly
+                        sy -= ofy[qq];
+                        sz -= ofz[qq];
+                        const int nb = static_cast<int>(pnb[d] & 0x1FFu);
+                        if (nb >= kH0) {  // lower endpoint in this CTA
+                            F[(3 * d) * kNmp + nb - kH0] = ofx[qq];
+                            F[(3 * d + 1) * kNmp + nb - kH0] = ofy[qq];
+                            F[(3 * d + 2) * kNmp + nb - kH0] = ofz[qq];
+                        } else {  // in the previous CTA: its slot index there is nb - kH0 + q
+                            const uint32_t o = f_prev + 8u * static_cast<uint32_t>((3 * d) * kNmp + nb - kH0 + q);
+                            st_remote(o, ofx[qq]);
+                            st_remote(o + 8u * kNmp, ofy[qq]);
+                            st_remote(o + 16u * kNmp, ofz[qq]);
+                        }
+                    }
+                }
+            }
+        }
+        ++steps;
+        if (zero_len) raise_flag(tag1);
+        cluster_barrier();
+        if (*reinterpret_cast<volatile uint32_t*>(&s_flag) == tag1) {  // step() returns diverged
+            diverged = 1;
+            break;
+        }
+        ++ok_phase1;
+        // ---- phase 2: ascending spring index = backward d = 12..0, forward d = 0..12
+        int bad = 0;
+        if (live) {
+            double fx = sx, fy = sy, fz = sz;
+#pragma unroll
+            for (int d = 0; d < 13; ++d) {
+                if (fmask & (1u << d)) {
+                    fx += F[(3 * d) * kNmp + a];
+                    fy += F[(3 * d + 1) * kNmp + a];
+                    fz += F[(3 * d + 2) * kNmp + a];
+                }
+            }
+            if (en_grav) fz -= mg;
+            if (en_contact && x2 < 0.0) {
+                const double penetration = -x2;
+                double normal = plane_k * penetration - gdmp * v2;
+                if (normal < 0.0) normal = 0.0;
+                const double ft_norm = sqrt(fx * fx + fy * fy);
+                const double vt_norm = sqrt(v0 * v0 + v1 * v1);
+                if (vt_norm < kStickVelocity && ft_norm <= mu_s * normal) {
+                    fx = 0.0;
+                    fy = 0.0;
+                } else if (vt_norm > 0.0) {
+                    const double scale = mu_k * normal / vt_norm;
+                    fx -= scale * v0;
+                    fy -= scale * v1;
+                } else if (ft_norm > 0.0) {
+                    const double scale = mu_k * normal / ft_norm;
+                    fx -= scale * fx;
+                    fy -= scale * fy;
+                }
+                fz += normal;
+            }
+            v0 += fx * imdt;
+            v1 += fy * imdt;
+            v2 += fz * imdt;
+            x0 += v0 * dt;
+            x1 += v1 * dt;
+            x2 += v2 * dt;
+            X[kH0 + a] = x0;
+            X[kXS + kH0 + a] = x1;
+            X[2 * kXS + kH0 + a] = x2;
+            X[3 * kXS + kH0 + a] = v0;
+            X[4 * kXS + kH0 + a] = v1;
+            X[5 * kXS + kH0 + a] = v2;
+            if (push_halo) {  // the next CTA's halo copy of this mass
+                const uint32_t o = x_next + 8u * static_cast<uint32_t>(g - (lo + q) + kH0);
+                st_remote(o, x0);
+                st_remote(o + 8u * kXS, x1);
+                st_remote(o + 16u * kXS, x2);
+                st_remote(o + 24u * kXS, v0);
+                st_remote(o + 32u * kXS, v1);
+                st_remote(o + 40u * kXS, v2);
+            }
+            const double speed_sq = v0 * v0 + v1 * v1 + v2 * v2;
+            if (speed_sq > max_sq) max_sq = speed_sq;
+            if (!(fabs(x0) <= kDivergenceBound) || !(fabs(x1) <= kDivergenceBound) ||
+                !(fabs(x2) <= kDivergenceBound))
+                bad = 1;
+        }
+        if (kstep + 1 < A.n_steps) {  // drive of the next step, per voxel
+            const double2 drv = __ldg(A.drive + kstep + 1);
+#pragma unroll
+            for (int j = 0; j < kVpt; ++j) {
+                const int v = a + j * kNmp;
+                if (v < NT) D[v] = drv.x * vcos[j] + drv.y * vsin[j];
+            }
+        }
+        if (bad) raise_flag(tag2);
+        cluster_barrier();
+        if (*reinterpret_cast<volatile uint32_t*>(&s_flag) == tag2) {
+            diverged = 1;
+            break;
+        }
+    }
+
+    // ---------------------------------------------------------- summary
+    for (int o = 16; o > 0; o >>= 1) {
+        const double other = __shfl_xor_sync(0xffffffffu, max_sq, o);
+        if (other > max_sq) max_sq = other;
+    }
+    if ((a & 31) == 0) s_maxsq[a >> 5] = max_sq;
+    if (live) {
+        for (int c = 0; c < 3; ++c) {
+            A.xfinal[c * b.M + mo + g] = X[c * kXS + kH0 + a];
+            A.xfinal[(3 + c) * b.M + mo + g] = X[(3 + c) * kXS + kH0 + a];
+            if (A.write_back) {
+                b.pos[c * b.M + mo + g] = X[c * kXS + kH0 + a];
+                b.vel[c * b.M + mo + g] = X[(3 + c) * kXS + kH0 + a];
+            }
+        }
+    }
+    __syncthreads();
+    if (a == 0) {
+        double m = 0.0;
+        for (int w = 0; w < kNmp / 32; ++w)
+            if (s_maxsq[w] > m) m = s_maxsq[w];
+        st_remote(map_rank(smem_addr(&s_cmax[rank]), 0u), m);
+    }
+    __threadfence();   // final state visible to rank 0 (global memory)
+    cluster_barrier();
+    if (out && a == 0) {
+        double m = 0.0;
+        for (int c = 0; c < cl; ++c)
+            if (s_cmax[c] > m) m = s_cmax[c];
+        double c0 = 0.0, c1 = 0.0, c2 = 0.0, total = 0.0;
+        for (int mm = 0; mm < nm; ++mm) {
+            const double w = b.mass[mo + mm];
+            c0 += w * A.xfinal[mo + mm];
+            c1 += w * A.xfinal[b.M + mo + mm];
+            c2 += w * A.xfinal[2 * b.M + mo + mm];
+            total += w;
+        }
+        if (total > 0.0) {
+            c0 /= total;
+            c1 /= total;
+            c2 /= total;
+        }
+        const double com_end[3] = {c0, c1, c2};
+        for (int c = 0; c < 3; ++c) {
+            out->com_start[c] = com_start[c];
+            out->com_end[c] = com_end[c];
+        }
+        const double dx = com_end[0] - com_start[0];
+        const double dy = com_end[1] - com_start[1];
+        out->horizontal_displacement = sqrt(dx * dx + dy * dy);
+        out->max_speed = sqrt(m);
+        out->diverged = diverged;
+        out->steps = steps;
+        out->spring_updates = static_cast<uint64_t>(ok_phase1) * static_cast<uint64_t>(b.nspring[r]);
+    }
+}
+
+size_t cluster_smem(int ncell) { return (6ull * kXS + 65ull * kNmp + 2ull * (ncell + 1)) * sizeof(double); }
+
+int cluster_size_for(int nm_max) { return (nm_max + kNmp - 2) / (kNmp - 1); }
+
+}  // namespace
+
+// false when the batch is not a device-built lattice batch of the size this
+// kernel covers; the caller then uses the streaming kernel.
+bool cluster_applicable(vx_ctx* ctx, vx_batch* b) {
+    if (!b->lattice || !b->vkey.p || !b->act_vox.p) return false;
+    static const char* force = std::getenv("VX_INTEGRATOR");  // "stream" / "generic" skip this kernel
+    if (force && (std::string(force) == "stream" || std::string(force) == "generic")) return false;
+    const int ncell = b->lw * b->lh * b->ld;
+    const int halo = (b->lw + 1) * (b->lh + 1) + (b->lw + 1) + 1;
+    const int cl = cluster_size_for(b->nm_max);
+    if (cl < 2 || cl > kMaxCluster || halo > kH0 || ncell + 1 > kVpt * kNmp) return false;
+    if (cluster_smem(ncell) + 1024 > ctx->smem_optin) return false;
+    if (ctx->cluster_ok < 0) {  // can a cluster of kMaxCluster such CTAs be co-scheduled?
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(kMaxCluster);
+        cfg.blockDim = dim3(kNmp);
+        cfg.dynamicSmemBytes = cluster_smem(kVpt * kNmp - 1);
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = kMaxCluster;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        int n = 0;
+        const bool ok = cudaFuncSetAttribute(cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(cfg.dynamicSmemBytes)) == cudaSuccess &&
+                        cudaOccupancyMaxActiveClusters(&n, cluster_kernel, &cfg) == cudaSuccess && n > 0;
+        cudaGetLastError();
+        ctx->cluster_ok = ok ? 1 : 0;
+    }
+    return ctx->cluster_ok == 1;
+}
+
+vx_status integrate_cluster(vx_ctx* ctx, vx_batch* b, int64_t n_steps, bool write_back, vx_summary* d_summaries,
+                            const SimParams& sp, double zero_len2) {
+    ClArgs A{};
+    A.b = view_of(b);
+    A.vkey = b->vkey.p;
+    A.act_vox = b->act_vox.p;
+    A.sign = b->sign.p;
+    A.amp = b->amp.p;
+    A.drive = ctx->drive.p;
+    A.sp = sp;
+    A.n_steps = n_steps;
+    A.write_back = write_back ? 1 : 0;
+    A.out = d_summaries;
+    A.cl = cluster_size_for(b->nm_max);
+    A.halo = (b->lw + 1) * (b->lh + 1) + (b->lw + 1) + 1;
+    A.vw = b->lw + 1;
+    A.vh = b->lh + 1;
+    A.ncell = b->lw * b->lh * b->ld;
+    A.zero_len2 = zero_len2;
+    VX_TRY(ctx->cluster_state.alloc(6 * static_cast<size_t>(b->M)));
+    A.xfinal = ctx->cluster_state.p;
+    const size_t smem = cluster_smem(A.ncell);
+    VX_CUDA(cudaFuncSetAttribute(cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(static_cast<unsigned>(b->n * A.cl));
+    cfg.blockDim = dim3(kNmp);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = ctx->stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = static_cast<unsigned>(A.cl);
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    VX_CUDA(cudaLaunchKernelEx(&cfg, cluster_kernel, A));
+    ctx->launches++;
+    return VX_OK;
+}
+
+}  // namespace vx
