@@ -73,6 +73,12 @@ __device__ __forceinline__ uint32_t map_rank(uint32_t addr, uint32_t rank) {
 __device__ __forceinline__ void st_remote(uint32_t addr, double v) {
     asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(addr), "d"(v));
 }
+// predicated DSMEM store (no branch around the asm, so the chunk stays straight-line code)
+__device__ __forceinline__ void st_remote_if(bool p, uint32_t addr, double v) {
+    asm volatile(
+        "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q st.shared::cluster.f64 [%0], %1;\n\t}" ::"r"(addr),
+        "d"(v), "r"(static_cast<int>(p)));
+}
 __device__ __forceinline__ void st_remote_u32(uint32_t addr, uint32_t v) {
     asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(addr), "r"(v));
 }
@@ -318,22 +324,25 @@ __global__ void __launch_bounds__(kNmp, 1) cluster_kernel(ClArgs A) {
                 for (int qq = 0; qq < kChunk; ++qq) {
                     const int d = c0 - qq;
                     if (d < 0) break;
-                    if ((bmask >> d) & 1u) {
+                    const bool valid = (bmask >> d) & 1u;
+                    if (valid) {
                         sx -= ofx[qq];  // fx += (-1)*F == fx - F exactly
                         sy -= ofy[qq];
                         sz -= ofz[qq];
-                        const int nb = static_cast<int>(pnb[d] & 0x1FFu);
-                        if (nb >= kH0) {  // lower endpoint in this CTA
-                            F[(3 * d) * kNmp + nb - kH0] = ofx[qq];
-                            F[(3 * d + 1) * kNmp + nb - kH0] = ofy[qq];
-                            F[(3 * d + 2) * kNmp + nb - kH0] = ofz[qq];
-                        } else {  // in the previous CTA: its slot index there is nb - kH0 + q
-                            const uint32_t o = f_prev + 8u * static_cast<uint32_t>((3 * d) * kNmp + nb - kH0 + q);
-                            st_remote(o, ofx[qq]);
-                            st_remote(o + 8u * kNmp, ofy[qq]);
-                            st_remote(o + 16u * kNmp, ofz[qq]);
-                        }
                     }
+                    // lower endpoint in this CTA (X index >= kH0) or in the previous
+                    // one, where its slot index is nb - kH0 + q: predicated, no branch
+                    const int li = static_cast<int>(pnb[d] & 0x1FFu) - kH0;
+                    const bool rem = li < 0;
+                    if (valid && !rem) {
+                        F[(3 * d) * kNmp + li] = ofx[qq];
+                        F[(3 * d + 1) * kNmp + li] = ofy[qq];
+                        F[(3 * d + 2) * kNmp + li] = ofz[qq];
+                    }
+                    const uint32_t o = f_prev + 8u * static_cast<uint32_t>((3 * d) * kNmp + li + q);
+                    st_remote_if(valid && rem, o, ofx[qq]);
+                    st_remote_if(valid && rem, o + 8u * kNmp, ofy[qq]);
+                    st_remote_if(valid && rem, o + 16u * kNmp, ofz[qq]);
                 }
             }
         }
