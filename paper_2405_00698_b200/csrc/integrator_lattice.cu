@@ -9,17 +9,18 @@
 //    "forward" directions d (ascending key offset == ascending j, i.e. the
 //    reference's (i, j) spring order).  Thread a owns the <= 13 BACKWARD
 //    springs (a - off_d, a) of mass a (it is their higher endpoint) and keeps
-//    their k / neighbour / actuating voxel, its forward neighbours and its
-//    per-mass constants in REGISTERS for the whole launch (rest0 and c in
-//    direction-major shared memory), its own mass state in registers;
+//    their k / neighbour / actuating voxel and its per-mass constants in
+//    REGISTERS for the whole launch (rest0 and c in direction-major shared
+//    memory), its own mass state in registers;
 //  * phase 1 computes those springs for d = 12..0 (= ascending i = ascending
 //    spring index): the reference's ordered gather for mass a begins with
 //    exactly these terms (fx = 0.0; fx += (-1)*F_s), so thread a accumulates
 //    them in registers as it goes and stores each force ONCE, to the
-//    direction-major slot F[d][a], for the lower endpoint — neighbour loads
+//    direction-major slot F[d][i] of the LOWER endpoint i — neighbour loads
 //    and slot stores of a warp touch consecutive addresses (no conflicts);
+//    a chunk of directions no lane of the warp has is skipped;
 //  * phase 2 continues mass a's sum with its forward springs d = 0..12
-//    (ascending j), reading F[d][a + off_d] — completing the reference's
+//    (ascending j), reading its own contiguous slots F[d][a] — completing the reference's
 //    ascending-spring-index CSR order (physics.hpp:166-184, 219-225) — then
 //    gravity / contact / integrate; the
 //    per-voxel drive D_v = sin(wt)cos(phi_v) + cos(wt)sin(phi_v) of the next
@@ -31,6 +32,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <string>
+#include <type_traits>
 
 #include "vx_internal.cuh"
 
@@ -129,7 +131,6 @@ __global__ void __launch_bounds__(NMP, 1) lattice_kernel(LatArgs A) {
     }
     double pk[13];
     uint32_t pnb[13];  // backward (lower) neighbour | actuating voxel << 16 (ncell = passive/missing)
-    uint32_t fnb[7];   // forward (higher) neighbours, two u16 per word
     unsigned fmask = 0u, bmask = 0u;
     double mg = 0.0, imdt = 0.0, gdmp = 0.0;
     double x0 = 0.0, x1 = 0.0, x2 = 0.0, v0 = 0.0, v1 = 0.0, v2 = 0.0;
@@ -140,8 +141,6 @@ __global__ void __launch_bounds__(NMP, 1) lattice_kernel(LatArgs A) {
         PR[d * NMP + a] = 1.0;
         PC[d * NMP + a] = 0.0;
     }
-#pragma unroll
-    for (int q = 0; q < 7; ++q) fnb[q] = 0u;
     if (a == NMP - 1) {  // ghost mass: far from every real mass, at rest; missing
         X[a] = 1e3;      // springs point at it so every slot runs the same
         X[NMP + a] = 1e3;  // branch-free code on the sqrt/div fast paths
@@ -191,14 +190,14 @@ __global__ void __launch_bounds__(NMP, 1) lattice_kernel(LatArgs A) {
                         PC[d * NMP + a] = b.c[so + s];
                         const int av = A.act_vox[so + s];
                         pnb[d] = static_cast<uint32_t>(other) | (static_cast<uint32_t>(av >= 0 ? av : A.ncell) << 16);
-                    } else {      // spring (a, other): computed by `other`, read back in phase 2
+                    } else {      // spring (a, other): `other` computes it and stores F[d][a]
                         fmask |= 1u << d;
-                        fnb[d >> 1] |= static_cast<uint32_t>(other) << (16 * (d & 1));
                     }
                 }
             }
         }
     }
+    const unsigned wmask = __reduce_or_sync(0xffffffffu, bmask);  // directions any lane of the warp has
     __syncthreads();
     {
         const double2 drv = __ldg(A.drive);
@@ -232,14 +231,15 @@ __global__ void __launch_bounds__(NMP, 1) lattice_kernel(LatArgs A) {
         int zero_len = 0;
         double sx = 0.0, sy = 0.0, sz = 0.0;
         const double* __restrict__ Xr = X;
-        constexpr int kChunk = 5;
+        // chunks d = 12..9 | 8..4 | 3..0 (the dz = +1 pairs, the rest of dz = +1, the
+        // in-plane directions); a chunk no lane of the warp has a spring in is
+        // skipped (warp-uniform branch): z = 0 plane warps skip two of three
+        auto chunk = [&](auto c0_tag, auto n_tag) {
+            constexpr int c0 = decltype(c0_tag)::value, n = decltype(n_tag)::value;
+            double ofx[n], ofy[n], ofz[n];
 #pragma unroll
-        for (int c0 = 12; c0 >= 0; c0 -= kChunk) {
-            double ofx[kChunk], ofy[kChunk], ofz[kChunk];
-#pragma unroll
-            for (int q = 0; q < kChunk; ++q) {
-                const int d = c0 - q;
-                if (d < 0) break;
+            for (int qq = 0; qq < n; ++qq) {
+                const int d = c0 - qq;
                 const bool valid = (bmask >> d) & 1u;
                 const int nb = static_cast<int>(pnb[d] & 0xFFFFu);
                 const int vox = static_cast<int>(pnb[d] >> 16);
@@ -257,24 +257,29 @@ __global__ void __launch_bounds__(NMP, 1) lattice_kernel(LatArgs A) {
                 const double rel = (v0 - Xr[3 * NMP + nb]) * nx + (v1 - Xr[4 * NMP + nb]) * ny +
                                    (v2 - Xr[5 * NMP + nb]) * nz;
                 const double mag = pk[d] * (len - rest) + PC[d * NMP + a] * rel;
-                ofx[q] = mag * nx;
-                ofy[q] = mag * ny;
-                ofz[q] = mag * nz;
+                ofx[qq] = mag * nx;
+                ofy[qq] = mag * ny;
+                ofz[qq] = mag * nz;
             }
 #pragma unroll
-            for (int q = 0; q < kChunk; ++q) {
-                const int d = c0 - q;
-                if (d < 0) break;
+            for (int qq = 0; qq < n; ++qq) {
+                const int d = c0 - qq;
                 if ((bmask >> d) & 1u) {
-                    sx -= ofx[q];  // fx += (-1)*F == fx - F exactly
-                    sy -= ofy[q];
-                    sz -= ofz[q];
-                    F[(3 * d) * NMP + a] = ofx[q];
-                    F[(3 * d + 1) * NMP + a] = ofy[q];
-                    F[(3 * d + 2) * NMP + a] = ofz[q];
+                    sx -= ofx[qq];  // fx += (-1)*F == fx - F exactly
+                    sy -= ofy[qq];
+                    sz -= ofz[qq];
+                    const int nb = static_cast<int>(pnb[d] & 0xFFFFu);  // slot of the LOWER endpoint
+                    F[(3 * d) * NMP + nb] = ofx[qq];
+                    F[(3 * d + 1) * NMP + nb] = ofy[qq];
+                    F[(3 * d + 2) * NMP + nb] = ofz[qq];
                 }
             }
-        }
+        };
+        using I4 = std::integral_constant<int, 4>;
+        using I5 = std::integral_constant<int, 5>;
+        if (wmask & 0x1E00u) chunk(std::integral_constant<int, 12>{}, I4{});
+        if (wmask & 0x01F0u) chunk(std::integral_constant<int, 8>{}, I5{});
+        if (wmask & 0x000Fu) chunk(std::integral_constant<int, 3>{}, I4{});
         ++steps;
         if (__syncthreads_or(zero_len)) {  // step() returns diverged; masses untouched
             diverged = 1;
@@ -289,11 +294,10 @@ __global__ void __launch_bounds__(NMP, 1) lattice_kernel(LatArgs A) {
             double fx = sx, fy = sy, fz = sz;
 #pragma unroll
             for (int d = 0; d < 13; ++d) {
-                if (fmask & (1u << d)) {
-                    const int nb = static_cast<int>((fnb[d >> 1] >> (16 * (d & 1))) & 0xFFFFu);
-                    fx += F[(3 * d) * NMP + nb];
-                    fy += F[(3 * d + 1) * NMP + nb];
-                    fz += F[(3 * d + 2) * NMP + nb];
+                if (fmask & (1u << d)) {  // F[d][a]: force on a of spring (a, a + off_d)
+                    fx += F[(3 * d) * NMP + a];
+                    fy += F[(3 * d + 1) * NMP + a];
+                    fz += F[(3 * d + 2) * NMP + a];
                 }
             }
             if (en_grav) fz -= mg;
