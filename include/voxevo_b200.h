@@ -313,7 +313,7 @@ vx_status vx_integrator_timing(vx_ctx* ctx, double* total_ms, int64_t* n_launche
 vx_status vx_fp64_peak(vx_ctx* ctx, double* tflops);
 /* Self-check of the integrator's branch-free sqrt / reciprocal against the
  * IEEE sqrt(x) and 1.0/x over n pseudo-random inputs spanning the ranges the
- * integrator feeds them (plus powers of two and their neighbours);
+ * integrator feeds them (plus powers of two and a few ulps around them);
  * mismatches[0] = sqrt, mismatches[1] = rcp. */
 vx_status vx_fastmath_check(vx_ctx* ctx, int64_t n, uint64_t seed, int64_t* mismatches);
 

@@ -373,7 +373,8 @@ class Context:
         return float(t.value)
 
     def fastmath_check(self, n: int, seed: int = 1) -> tuple:
-        """Mismatches (sqrt, rcp) of the integrator's branch-free sqrt/rcp vs IEEE over n samples."""
+        """Mismatches (sqrt, rcp) of the integrator's branch-free sqrt / reciprocal
+        vs IEEE sqrt and division over n samples."""
         out = np.zeros(2, np.int64)
         _check(_lib().vx_fastmath_check(self.h, n, seed, out.ctypes.data))
         return int(out[0]), int(out[1])

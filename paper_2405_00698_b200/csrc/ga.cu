@@ -137,8 +137,8 @@ __global__ void stats_kernel(int P, const double* sorted_fit, double* out3) {
 // next[c] for every slot: elites copy sorted[c]; children copy sorted[pa],
 // overwritten by sorted[pb] where the crossover mask bit is set.
 __global__ void breed_kernel(BreedArgs A) {
-    const int c = blockIdx.y;
-    const int64_t i0 = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int c = blockIdx.x;  // child slot (gridDim.x: up to 2^31-1 individuals)
+    const int64_t i0 = static_cast<int64_t>(blockIdx.y) * blockDim.x + threadIdx.x;
     int src_a, src_b = -1;
     const uint32_t* mask = nullptr;
     if (c < A.n_elite) {
@@ -151,16 +151,16 @@ __global__ void breed_kernel(BreedArgs A) {
             mask = A.masks + static_cast<int64_t>(p.mask_slot) * A.mask_words;
         }
     }
-    for (int64_t i = i0; i < A.np; i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    for (int64_t i = i0; i < A.np; i += static_cast<int64_t>(gridDim.y) * blockDim.x) {
         double v = A.src_params[static_cast<int64_t>(src_a) * A.np + i];
         if (mask && ((mask[i >> 5] >> (i & 31)) & 1u)) v = A.src_params[static_cast<int64_t>(src_b) * A.np + i];
         A.dst_params[static_cast<int64_t>(c) * A.np + i] = v;
     }
-    for (int64_t i = i0; i < A.nb; i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    for (int64_t i = i0; i < A.nb; i += static_cast<int64_t>(gridDim.y) * blockDim.x)
         A.dst_bmat[static_cast<int64_t>(c) * A.nb + i] = A.src_bmat[static_cast<int64_t>(src_a) * A.nb + i];
     if (c < A.n_elite) {
         // elites keep fitness, evaluated flag and cached raw grid
-        for (int64_t i = i0; i < A.cells; i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        for (int64_t i = i0; i < A.cells; i += static_cast<int64_t>(gridDim.y) * blockDim.x) {
             A.dst_grid[static_cast<int64_t>(c) * A.cells + i] = A.src_grid[static_cast<int64_t>(src_a) * A.cells + i];
             A.dst_gridw[static_cast<int64_t>(c) * A.cells + i] =
                 A.src_gridw[static_cast<int64_t>(src_a) * A.cells + i];
@@ -241,7 +241,7 @@ vx_status sort_stats_dev(vx_ctx* ctx, int P, const double* d_fit, int32_t* d_per
 }
 
 vx_status breed_dev(vx_ctx* ctx, const BreedArgs& A, int P, const MutEntry* d_mut, int64_t n_mut) {
-    dim3 grid(ceil_div(A.np, kThreads) < 64 ? ceil_div(A.np, kThreads) : 64, P);
+    dim3 grid(P, ceil_div(A.np, kThreads) < 64 ? ceil_div(A.np, kThreads) : 64);
     breed_kernel<<<grid, kThreads, 0, ctx->stream>>>(A);
     ctx->launches++;
     VX_CUDA(cudaGetLastError());

@@ -37,6 +37,8 @@ __device__ double sample_range(uint64_t h, int emin, int emax) {
     const int e = emin + static_cast<int>((h >> 52) % static_cast<uint64_t>(emax - emin + 1));
     uint64_t mant = h & 0xFFFFFFFFFFFFFULL;
     if ((h & 0xF0000000000000ULL) == 0) mant = (h & 1) ? 0 : 0xFFFFFFFFFFFFFULL;
+    if ((h & 0xF0000000000000ULL) == 0x10000000000000ULL)  // a few ulps above / below a power of two
+        mant = (h & 2) ? ((h >> 20) & 0xFFFF) : 0xFFFFFFFFFFFFFULL - ((h >> 20) & 0xFFFF);
     const uint64_t bits = (static_cast<uint64_t>(e + 1023) << 52) | mant;
     return __longlong_as_double(static_cast<long long>(bits));
 }
@@ -53,6 +55,7 @@ __global__ void fastmath_kernel(int64_t n, uint64_t seed, unsigned long long* ba
     }
     if (bs) atomicAdd(bad, bs);
     if (br) atomicAdd(bad + 1, br);
+
 }
 
 }  // namespace
@@ -72,6 +75,7 @@ vx_status vx_fastmath_check(vx_ctx* ctx, int64_t n, uint64_t seed, int64_t* mism
     VX_CUDA(cudaStreamSynchronize(ctx->stream));
     mismatches[0] = static_cast<int64_t>(h[0]);
     mismatches[1] = static_cast<int64_t>(h[1]);
+
     return VX_OK;
 }
 

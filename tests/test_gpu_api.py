@@ -120,3 +120,14 @@ def test_empty_and_passive_robots_in_population(vx, ctx):
     st.set_population(zero, pop["bmat"])  # all-zero MLP -> five-way tie -> Empty everywhere
     r = st.evolve_generation()
     assert r.best == 0.0 and r.mean == 0.0 and r.spring_updates == 0
+
+
+def test_population_beyond_grid_y_limit(vx, ctx):
+    # config 4 runs P = 65536: every per-individual launch must take P > 65535
+    cfg = vx.EvolutionConfig(population=70000, generations=1, grid=(2, 2, 2), hidden_widths=[4], m=4, seed=3,
+                             sim=vx.SimConfig(dt=1e-4, duration=1e-3))
+    st = vx.init_evolution(cfg, ctx)
+    r0 = st.evolve_generation()
+    r1 = st.evolve_generation()
+    assert r0.evaluations == 70000 and r1.evaluations == 70000 - vx.elite_count(0.3, 70000)
+    assert r1.best >= r0.best
