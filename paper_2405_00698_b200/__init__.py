@@ -753,3 +753,4 @@ def report_dict(r: GenerationReport) -> dict:
 # config files and checkpoints (config.hpp / serialize.hpp formats)
 from .serialize import (CheckpointError, ConfigError, RunConfig, curves_csv, load_genome, load_run,  # noqa: E402
                         load_run_config, run_config_from_json, save_genome, save_run, write_curves_csv)
+from .runner import ScriptedAdvisor, resume_run, run_config_to_json, run_loop, start_run  # noqa: E402

@@ -35,6 +35,13 @@ from . import (NMAT, Arch, Context, EvolutionConfig, EvolutionState, GenerationR
 CHECKPOINT_MAGIC = "voxevo"  # kCheckpointMagic (serialize.hpp:20)
 CHECKPOINT_VERSION = 1       # kCheckpointVersion (serialize.hpp:21)
 ADVISORS = ("off", "scripted", "llm", "replay")
+# LlmAdvisorConfig defaults (advisor_http.hpp:22-34): parsed and echoed, never contacted
+LLM_DEFAULTS = {"url": "http://127.0.0.1:8080", "path": "/v1/chat/completions", "model": "advisor-model",
+                "api_key_env": "VOXEVO_LLM_KEY", "temperature": 0.0, "max_retries": 2, "backoff_base_ms": 1000,
+                "connect_timeout_s": 5, "read_timeout_s": 30, "allow_material_multipliers": False,
+                "audit_path": ""}
+_LLM_KIND = {"temperature": float, "max_retries": int, "backoff_base_ms": int, "connect_timeout_s": int,
+             "read_timeout_s": int, "allow_material_multipliers": bool}
 
 
 class ConfigError(RuntimeError):
@@ -176,11 +183,11 @@ def _get(j: dict, key: str, default, kind=None):
 
 @dataclass
 class RunConfig:
-    """RunConfig (config.hpp:19-26).  ``llm`` keeps the raw LLM-advisor block
+    """RunConfig (config.hpp:19-26).  ``llm`` holds the LlmAdvisorConfig fields
     (the HTTP advisor itself is out of scope)."""
     evolution: EvolutionConfig = field(default_factory=EvolutionConfig)
     advisor: str = "off"
-    llm: dict = field(default_factory=dict)
+    llm: dict = field(default_factory=lambda: dict(LLM_DEFAULTS))
     replay_audit: str = ""
     out_dir: str = "runs/latest"
     checkpoint_stride: int = 1
@@ -235,7 +242,8 @@ def run_config_from_json(j: Any) -> RunConfig:
     if rc.advisor not in ADVISORS:
         raise ConfigError("advisor must be off, scripted, llm, or replay")
     if "llm" in j:
-        rc.llm = dict(j["llm"])
+        for key, default in LLM_DEFAULTS.items():
+            rc.llm[key] = _get(j["llm"], key, default, _LLM_KIND.get(key, str))
     rc.replay_audit = _get(j, "replay_audit", rc.replay_audit, str)
     rc.out_dir = _get(j, "out_dir", rc.out_dir, str)
     rc.checkpoint_stride = _get(j, "checkpoint_stride", rc.checkpoint_stride, int)
@@ -243,15 +251,10 @@ def run_config_from_json(j: Any) -> RunConfig:
 
 
 def load_run_config(path: str) -> RunConfig:
-    """Read a hand-written run-config file (config.hpp:31)."""
-    try:
-        with open(path, "rb") as f:
-            j = json.loads(f.read())
-    except OSError as exc:
-        raise ConfigError(f"cannot open: {path}") from exc
-    except ValueError as exc:
-        raise ConfigError(f"invalid JSON: {path}") from exc
-    return run_config_from_json(j)
+    """load_run_config (config.hpp:150-152): the file is read by
+    load_json_file, so an unreadable file or bad JSON is a CheckpointError and
+    a bad value a ConfigError, as in the reference."""
+    return run_config_from_json(load_json_file(path))
 
 
 # ---------------------------------------------------- component serializers

@@ -175,9 +175,9 @@ def test_run_config_errors(S, tmp_path):
         S.run_config_from_json({"population": "many"})
     p = tmp_path / "bad.json"
     p.write_text("{not json")
-    with pytest.raises(S.ConfigError, match="invalid JSON"):
+    with pytest.raises(S.CheckpointError, match="invalid JSON"):  # load_json_file's error, as in the reference
         S.load_run_config(str(p))
-    with pytest.raises(S.ConfigError, match="cannot open"):
+    with pytest.raises(S.CheckpointError, match="cannot open"):
         S.load_run_config(str(tmp_path / "missing.json"))
     p.write_text(json.dumps({"population": 8, "grid": [4, 4, 4]}))
     assert S.load_run_config(str(p)).evolution.population == 8
