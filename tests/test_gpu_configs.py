@@ -1,0 +1,49 @@
+"""Every specialised integrator (one-SM lattice 6^3, cluster 10^3, streaming
+20^3) under non-default SimConfig / MaterialTable / GroundPlane settings:
+bit-exact against the reference's step() on identical systems
+(physics.hpp:191-264; scaled materials, plane and sim fields of
+morphology.hpp:45-65, 124-129 and physics.hpp:16-29)."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+KERNEL = {6: "lattice", 10: "cluster", 20: "stream"}
+STEPS = {6: 600, 10: 300, 20: 60}
+
+
+def _variants(vx):
+    return {
+        "free_fast_drive": (vx.SimConfig(enable_gravity=False, enable_contact=False, actuation_frequency=5.0),
+                            vx.MaterialTable(), vx.GroundPlane()),
+        "soft_slippery": (vx.SimConfig(dt=2e-5, gravity=5.0),
+                          vx.MaterialTable(k_muscle=3e3, k_soft=5e2, amp_max=0.4, phase_max=1.0, damping_ratio=0.2,
+                                           voxel_edge=0.05, mass_per_vertex=0.05),
+                          vx.GroundPlane(k=2e4, damping_ratio=0.3, mu_static=0.3, mu_kinetic=0.5)),
+        "fine_dt_sticky": (vx.SimConfig(dt=5e-6), vx.MaterialTable(k_bone=3e4),
+                           vx.GroundPlane(mu_static=1.5, mu_kinetic=1.2)),
+    }
+
+
+@pytest.mark.parametrize("n", [6, 10, 20])
+@pytest.mark.parametrize("variant", ["free_fast_drive", "soft_slippery", "fine_dt_sticky"])
+def test_specialised_integrators_nondefault(vx, ctx, orc, n, variant):
+    sim, table, plane = _variants(vx)[variant]
+    rng = np.random.default_rng(n)
+    g = orc.sample_genome(32, [64, 64], int(rng.integers(0, 2 ** 62)))
+    mats, wts = vx.decode(g[0][None], g[1][None], vx.Arch.make(), n, n, n, ctx)
+    items = [orc.bench_robot(n), (orc.largest_component(mats[0], n, n, n), wts[0])]
+    batch = vx.build_mass_spring(np.stack([m for m, _ in items]), np.stack([w for _, w in items]), n, n, n,
+                                 table=table, plane=plane, ctx=ctx)
+    systems = [orc.build(m, w, n, n, n, table.as_array(), plane.as_array()) for m, w in items]
+    batch.override_phase(np.concatenate([orc.workspace(s)["sin_phase"] for s in systems]),
+                         np.concatenate([orc.workspace(s)["cos_phase"] for s in systems]))
+    steps = STEPS[n]
+    out = batch.step(sim, 0, steps)
+    assert ctx.last_integrator == KERNEL[n]
+    got = batch.download()
+    for r, s in enumerate(systems):
+        ref, ok, called, upd, msq = orc.step(s, sim.as_array(), 0, steps)
+        np.testing.assert_array_equal(got.robot(r)["pos"], ref.pos, err_msg=f"{variant} grid {n} robot {r}")
+        np.testing.assert_array_equal(got.robot(r)["vel"], ref.vel, err_msg=f"{variant} grid {n} robot {r}")
+        assert out[r].spring_updates == upd and out[r].max_speed == np.sqrt(msq)
