@@ -231,9 +231,9 @@ __global__ void __launch_bounds__(NMP, 1) lattice_kernel(LatArgs A) {
         int zero_len = 0;
         double sx = 0.0, sy = 0.0, sz = 0.0;
         const double* __restrict__ Xr = X;
-        // chunks d = 12..9 | 8..4 | 3..0 (the dz = +1 pairs, the rest of dz = +1, the
-        // in-plane directions); a chunk no lane of the warp has a spring in is
-        // skipped (warp-uniform branch): z = 0 plane warps skip two of three
+        // direction chunks 12..10 | 9..7 | 6..4 | 3..0 (the last: in-plane); a
+        // chunk no lane of the warp has a spring in is skipped (warp-uniform
+        // branch): z = 0 plane warps skip three of four
         auto chunk = [&](auto c0_tag, auto n_tag) {
             constexpr int c0 = decltype(c0_tag)::value, n = decltype(n_tag)::value;
             double ofx[n], ofy[n], ofz[n];
@@ -275,10 +275,14 @@ __global__ void __launch_bounds__(NMP, 1) lattice_kernel(LatArgs A) {
                 }
             }
         };
+        // chunk sizes 3-3-3-4 measured best (profiles/README.md: 9.5e10 vs 9.1e10
+        // for 4-5-4 and 9.3e10 for 2-wide chunks); the in-plane directions 3..0
+        // are one chunk, so z = 0 plane warps run a single chunk
+        using I3 = std::integral_constant<int, 3>;
         using I4 = std::integral_constant<int, 4>;
-        using I5 = std::integral_constant<int, 5>;
-        if (wmask & 0x1E00u) chunk(std::integral_constant<int, 12>{}, I4{});
-        if (wmask & 0x01F0u) chunk(std::integral_constant<int, 8>{}, I5{});
+        if (wmask & 0x1C00u) chunk(std::integral_constant<int, 12>{}, I3{});
+        if (wmask & 0x0380u) chunk(std::integral_constant<int, 9>{}, I3{});
+        if (wmask & 0x0070u) chunk(std::integral_constant<int, 6>{}, I3{});
         if (wmask & 0x000Fu) chunk(std::integral_constant<int, 3>{}, I4{});
         ++steps;
         if (__syncthreads_or(zero_len)) {  // step() returns diverged; masses untouched

@@ -1,0 +1,10 @@
+# A/B the integrator variants built under _variants/vN (development aid).
+cd $GRAFT_REPO_ROOT
+cp paper_2405_00698_b200/_lib/libvoxevo_b200.so /tmp/main.so
+for rep in 1 2; do
+for v in $(ls _variants); do
+  cp _variants/$v/libvoxevo_b200.so paper_2405_00698_b200/_lib/libvoxevo_b200.so
+  echo -n "$v: "; timeout -s KILL 120 python scripts/profile_integrator.py --steps 5000 ${VARIANT_ARGS} 2>&1 | tail -1
+done
+done
+cp /tmp/main.so paper_2405_00698_b200/_lib/libvoxevo_b200.so
