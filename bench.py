@@ -301,7 +301,11 @@ def main():
                 "peak_source": "measured DFMA throughput on this GPU (vx_fp64_peak; MEASURED_PEAKS.json has no "
                                "FP64 entry), 2 flop/DFMA",
                 "algorithmic": f"{FLOPS_PER_UPDATE} FP64 flop + 1 sqrt + 1 div per spring update x "
-                               f"{local_upd} updates per launch"}
+                               f"{local_upd} updates per launch",
+                "fp64_pipe_busy_ncu": _ncu_field("fp64_pipe_pct"),
+                "note": "parity mode forbids FMA contraction and IEEE sqrt/1/x cost ~15 FP64 instructions for 2 "
+                        "counted flop, so the flop fraction is structurally capped near 40%; fp64_pipe_busy_ncu is "
+                        "the FP64-pipe utilisation of the same kernel from the committed ncu capture"}
 
     cpu = None
     if world == 1 and not args.no_cpu_baseline and not args.profile:
@@ -340,15 +344,20 @@ def main():
         dist.destroy_process_group()
 
 
-def _ncu_traffic():
-    """dram bytes per integrator launch from the committed ncu capture, if any."""
+def _ncu_field(key):
+    """A field of the committed ncu capture of the integrator (profiles/integrator_traffic.json)."""
     path = os.path.join(ROOT, "profiles", "integrator_traffic.json")
     if os.path.exists(path):
         try:
-            return json.load(open(path)).get("dram_bytes_per_launch")
+            return json.load(open(path)).get(key)
         except Exception:
             return None
     return None
+
+
+def _ncu_traffic():
+    """dram bytes per integrator launch from the committed ncu capture, if any."""
+    return _ncu_field("dram_bytes_per_launch")
 
 
 if __name__ == "__main__":
