@@ -27,6 +27,15 @@
 namespace vx {
 namespace {
 
+#ifndef VX_STREAM_THREADS
+#define VX_STREAM_THREADS 1024
+#endif
+constexpr int kStreamThreads = VX_STREAM_THREADS;  // threads per robot: 1024 (64 registers) measured best
+#ifndef VX_STREAM_CHUNK
+#define VX_STREAM_CHUNK 2
+#endif
+constexpr int kStreamChunk = VX_STREAM_CHUNK;      // springs evaluated together: 2 measured best at 1024 threads
+
 struct StreamLayout {
     int nmp, mpt, threads;
     size_t per_robot;  // bytes
@@ -36,7 +45,7 @@ struct StreamLayout {
 
 StreamLayout stream_layout(int nm_cap, int ncell) {
     StreamLayout L{};
-    L.mpt = (nm_cap + 1 + 511) / 512;                        // masses per thread (ghost included), <= 512 threads
+    L.mpt = (nm_cap + 1 + kStreamThreads - 1) / kStreamThreads;  // masses per thread (ghost included)
     L.nmp = (nm_cap + 1 + 32 * L.mpt - 1) / (32 * L.mpt) * (32 * L.mpt);
     L.threads = L.nmp / L.mpt;
     size_t o = 0;
@@ -175,7 +184,7 @@ __global__ void __launch_bounds__(1024) stream_prep_kernel(StreamArgs A) {
 }
 
 template <bool kXSmem>
-__global__ void __launch_bounds__(512, 1) stream_kernel(StreamArgs A) {
+__global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(StreamArgs A) {
     const int r = blockIdx.x;
     const BatchView& b = A.b;
     const StreamLayout& L = A.L;
@@ -264,10 +273,10 @@ __global__ void __launch_bounds__(512, 1) stream_kernel(StreamArgs A) {
             const unsigned bmask = MASK[a] >> 13;
             double sx = 0.0, sy = 0.0, sz = 0.0;
 #pragma unroll
-            for (int c0 = 12; c0 >= 0; c0 -= 4) {
-                double ofx[4], ofy[4], ofz[4];
+            for (int c0 = 12; c0 >= 0; c0 -= kStreamChunk) {
+                double ofx[kStreamChunk], ofy[kStreamChunk], ofz[kStreamChunk];
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
+                for (int q = 0; q < kStreamChunk; ++q) {
                     const int d = c0 - q;
                     if (d < 0) break;
                     const bool valid = (bmask >> d) & 1u;
@@ -297,7 +306,7 @@ __global__ void __launch_bounds__(512, 1) stream_kernel(StreamArgs A) {
                     ofz[q] = mag * nz;
                 }
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
+                for (int q = 0; q < kStreamChunk; ++q) {
                     const int d = c0 - q;
                     if (d < 0) break;
                     if ((bmask >> d) & 1u) {
