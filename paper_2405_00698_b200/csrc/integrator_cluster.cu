@@ -302,6 +302,7 @@ __global__ void __launch_bounds__(kNmp, 1) cluster_kernel(ClArgs A) {
                     const bool valid = (bmask >> d) & 1u;
                     const int nb = static_cast<int>(pnb[d] & 0x1FFu);
                     const int vox = static_cast<int>(pnb[d] >> 9);
+                    VX_DCHECK(nb >= kH0 - H && nb < kXS && vox < NT);
                     // spring_force_on_i with i = nb, j = g (physics.hpp:55-64, 201-212)
                     double dx = x0 - Xr[nb];
                     double dy = x1 - Xr[kXS + nb];
@@ -334,6 +335,7 @@ __global__ void __launch_bounds__(kNmp, 1) cluster_kernel(ClArgs A) {
                     // one, where its slot index is nb - kH0 + q: predicated, no branch
                     const int li = static_cast<int>(pnb[d] & 0x1FFu) - kH0;
                     const bool rem = li < 0;
+                    VX_DCHECK(!valid || (rem ? (rank > 0 && li + q >= 0 && li + q < kNmp) : li < kNmp));
                     if (valid && !rem) {
                         F[(3 * d) * kNmp + li] = ofx[qq];
                         F[(3 * d + 1) * kNmp + li] = ofy[qq];
@@ -400,6 +402,7 @@ __global__ void __launch_bounds__(kNmp, 1) cluster_kernel(ClArgs A) {
             X[4 * kXS + kH0 + a] = v1;
             X[5 * kXS + kH0 + a] = v2;
             if (push_halo) {  // the next CTA's halo copy of this mass
+                VX_DCHECK(g - (lo + q) + kH0 >= kH0 - H && g - (lo + q) + kH0 < kH0);
                 const uint32_t o = x_next + 8u * static_cast<uint32_t>(g - (lo + q) + kH0);
                 st_remote(o, x0);
                 st_remote(o + 8u * kXS, x1);

@@ -243,6 +243,7 @@ __global__ void __launch_bounds__(NMP, 1) lattice_kernel(LatArgs A) {
                 const bool valid = (bmask >> d) & 1u;
                 const int nb = static_cast<int>(pnb[d] & 0xFFFFu);
                 const int vox = static_cast<int>(pnb[d] >> 16);
+                VX_DCHECK(nb < NMP && vox < NT);
                 // spring_force_on_i with i = nb, j = a (physics.hpp:55-64, 201-212)
                 double dx = x0 - Xr[nb];
                 double dy = x1 - Xr[NMP + nb];

@@ -283,6 +283,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(StreamArgs A)
                     const uint32_t w = PNB[d * NMP + a];
                     const int nb = static_cast<int>(w & 0x3FFFu);
                     const int vox = static_cast<int>(w >> 14);
+                    VX_DCHECK(nb < NMP && vox <= A.ncell);
                     const double dx = x0 - X[nb];
                     const double dy = x1 - X[NMP + nb];
                     const double dz = x2 - X[2 * NMP + nb];
@@ -340,6 +341,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(StreamArgs A)
             for (int d = 0; d < 13; ++d) {
                 if (fmask & (1u << d)) {
                     const int nb = static_cast<int>((FNB[(d >> 1) * NMP + a] >> (16 * (d & 1))) & 0xFFFFu);
+                    VX_DCHECK(nb < NMP);
                     fx += F[(3 * d) * NMP + nb];
                     fy += F[(3 * d + 1) * NMP + nb];
                     fz += F[(3 * d + 2) * NMP + nb];
