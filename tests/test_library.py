@@ -66,3 +66,26 @@ def test_no_device_fails_loudly(vx):
         pytest.skip("a GPU is present")
     with pytest.raises(vx.DeviceUnavailable):
         vx.Context(0)
+
+
+def test_header_is_plain_c(tmp_path):
+    """include/voxevo_b200.h is a C ABI: it must compile as C99 and C++17 and
+    every struct must be standard-layout (no torch / C++ types leak in)."""
+    import shutil
+    import subprocess
+    inc = os.path.join(ROOT, "include")
+    src = tmp_path / "abi.c"
+    src.write_text('#include "voxevo_b200.h"\nint main(void) { vx_status s = VX_OK; return (int)s; }\n')
+    cc = shutil.which("gcc") or "/usr/bin/gcc"
+    r = subprocess.run([cc, "-std=c99", "-Wall", "-Werror", "-pedantic", "-fsyntax-only", "-I", inc, str(src)],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    cxx = shutil.which("g++") or "/usr/bin/g++"
+    srcpp = tmp_path / "abi.cpp"
+    srcpp.write_text('#include "voxevo_b200.h"\n#include <type_traits>\n'
+                     'static_assert(std::is_standard_layout<vx_summary>::value, "");\n'
+                     'static_assert(std::is_standard_layout<vx_evo_config>::value, "");\n'
+                     'int main() { return 0; }\n')
+    r = subprocess.run([cxx, "-std=c++17", "-Wall", "-Werror", "-fsyntax-only", "-I", inc, str(srcpp)],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
