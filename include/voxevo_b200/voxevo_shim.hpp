@@ -105,6 +105,32 @@ inline void flatten(const Genome& g, std::vector<double>& params) {
     for (const auto* t : g.param_tensors()) params.insert(params.end(), t->begin(), t->end());
 }
 
+// The inverse: a reference Genome (param_tensors order, genome.hpp:57-68) from
+// the flat device layout of one individual.
+inline Genome unflatten(const EvolutionConfig& cfg, const double* params, const double* bmat) {
+    Genome g;
+    g.spec = cfg.encoding;
+    g.b_matrix.assign(bmat, bmat + g.spec.m * g.spec.d);
+    auto layer = [&](std::size_t in, std::size_t out) {
+        Layer l;
+        l.in = in;
+        l.out = out;
+        l.w.assign(params, params + in * out);
+        params += in * out;
+        l.b.assign(params, params + out);
+        params += out;
+        return l;
+    };
+    std::size_t prev = 2 * g.spec.m;
+    for (const std::size_t w : cfg.hidden_widths) {
+        g.hidden.push_back(layer(prev, w));
+        prev = w;
+    }
+    g.head_material = layer(prev, 5);
+    g.head_weight = layer(prev, 1);
+    return g;
+}
+
 // decode (morphology.hpp:141-157)
 inline VoxelGrid decode(const Genome& g, int w, int h, int d, Device& dev = default_device()) {
     if (w < 1 || h < 1 || d < 1) throw std::invalid_argument("decode: dims must be positive");
@@ -309,6 +335,51 @@ class GpuEvolution {
         double b = 0.0;
         vx_evo_best(evo_, &b, nullptr);
         return b;
+    }
+    // Resume from a reference EvolutionState — e.g. voxevo::load_run
+    // (serialize.hpp:311-313): genomes, fitness / evaluated flags (grids are
+    // decoded again, as after a reference load), params, history, generation,
+    // best fitness / genome and the GA's RNG stream.
+    void load_state(const EvolutionState& st) {
+        set_population(st.population);
+        const vx_hyper h = to_c(st.params);
+        check(vx_evo_set_params(evo_, &h));
+        set_rng_state(st.rng.state());
+        history = st.history;
+        std::vector<double> bp;
+        if (st.best_genome) flatten(*st.best_genome, bp);
+        check(vx_evo_set_progress(evo_, st.generation, st.best_fitness, st.best_genome ? bp.data() : nullptr,
+                                  st.best_genome ? st.best_genome->b_matrix.data() : nullptr));
+    }
+    // The device state as a reference EvolutionState, ready for
+    // voxevo::save_run (serialize.hpp:307-309).
+    EvolutionState to_state() const {
+        EvolutionState st;
+        st.config = cfg_;
+        vx_hyper h;
+        check(vx_evo_get_params(evo_, &h));
+        st.params = from_c(h);
+        const vx_evo_config c = to_c(cfg_);
+        const std::size_t np = static_cast<std::size_t>(vx_param_count(&c.arch)), nb = 3 * cfg_.encoding.m;
+        const std::size_t P = static_cast<std::size_t>(cfg_.population);
+        std::vector<double> params(P * np), bmat(P * nb), fit(P);
+        std::vector<uint8_t> ev(P);
+        check(vx_evo_get_population(evo_, params.data(), bmat.data(), fit.data(), ev.data(), nullptr, nullptr));
+        for (std::size_t i = 0; i < P; ++i) {
+            Individual ind;
+            ind.genome = unflatten(cfg_, params.data() + i * np, bmat.data() + i * nb);
+            ind.fitness = fit[i];
+            ind.evaluated = ev[i] != 0;
+            st.population.push_back(std::move(ind));
+        }
+        st.history = history;
+        st.generation = vx_evo_generation_index(evo_);
+        std::vector<double> bp(np), bb(nb);
+        double bf = 0.0;
+        if (vx_evo_best_genome(evo_, &bf, bp.data(), bb.data())) st.best_genome = unflatten(cfg_, bp.data(), bb.data());
+        st.best_fitness = bf;
+        st.rng.set_state(rng_state());
+        return st;
     }
     std::vector<GenerationReport> history;
 

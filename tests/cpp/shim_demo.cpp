@@ -11,6 +11,7 @@
 
 #include "voxevo/bench.hpp"
 #include "voxevo/evolution.hpp"
+#include "voxevo/serialize.hpp"
 #include "voxevo_b200/voxevo_shim.hpp"
 
 using namespace voxevo;
@@ -93,6 +94,43 @@ int main() {
            "ref " + std::to_string(r0.best) + " gpu " + std::to_string(g0.best));
     report("evolve_generation: best non-decreasing, RNG stream identical", mono && gpu.rng_state() == st.rng.state(),
            std::to_string(cfg.generations + 1) + " generations");
+
+    // checkpoints: the GPU state through the reference's own save_run /
+    // load_run (serialize.hpp) resumes identically, and a CPU checkpoint
+    // resumes on the GPU with the same GA stream (draws are fitness-independent)
+    {
+        EvolutionConfig c2 = cfg;
+        c2.seed = 9;
+        b200::GpuEvolution a(c2);
+        EvolutionState s0 = init_evolution(c2);
+        a.set_population(s0.population);
+        a.set_rng_state(s0.rng.state());
+        for (int k = 0; k < 2; ++k) a.evolve_generation();
+        const std::string path = "/tmp/voxevo_b200_shim_ckpt.json";
+        save_run(path, a.to_state());
+        b200::GpuEvolution b(c2);
+        b.load_state(load_run(path));
+        bool same = true;
+        for (int k = 0; k < 2; ++k) {
+            const GenerationReport x = a.evolve_generation(), y = b.evolve_generation();
+            same = same && x.best == y.best && x.mean == y.mean && x.diversity == y.diversity &&
+                   x.generation == y.generation;
+        }
+        report("checkpoint: GPU state -> save_run -> load_run resumes identically",
+               same && a.rng_state() == b.rng_state() && a.best_fitness() == b.best_fitness(),
+               "generations 2..3 after the reload");
+        EvolutionState cpu = init_evolution(c2);
+        for (int k = 0; k < 2; ++k) evolve_generation(cpu);
+        save_run(path, cpu);
+        b200::GpuEvolution c(c2);
+        c.load_state(load_run(path));
+        const GenerationReport gq = c.evolve_generation();
+        const GenerationReport cq = evolve_generation(cpu);
+        report("checkpoint: CPU state resumes on the GPU, same GA stream",
+               gq.generation == cq.generation && gq.evaluations == cq.evaluations && c.rng_state() == cpu.rng.state(),
+               "generation " + std::to_string(gq.generation));
+        std::remove(path.c_str());
+    }
 
     BenchConfig bc;
     const BenchResult br = b200::run_bench(bc);
