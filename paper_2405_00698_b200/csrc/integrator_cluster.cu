@@ -490,9 +490,425 @@ __global__ void __launch_bounds__(kNmp, 1) cluster_kernel(ClArgs A) {
     }
 }
 
+// ---------------------------------------------------------------------------
+// cluster_vertex_kernel<N>: the same cluster algorithm for N^3 grids with
+// threads indexed by LATTICE VERTEX KEY (see vertex_kernel in
+// integrator_lattice.cu): CTA c owns keys [c q, c q + q), every neighbour is
+// at a compile-time key offset (halo included: the state rows start PAD keys
+// below the range), absent vertices are idle threads parked far away.
+template <int N>
+struct ClusterGeom {
+    static constexpr int VW = N + 1;
+    static constexpr int NV = VW * VW * VW;
+    static constexpr int CL = (NV + kNmp - 2) / (kNmp - 1);     // CTAs per robot
+    static constexpr int Q = (NV + CL - 1) / CL;                  // keys per CTA
+    static constexpr int PAD = VW * VW + VW + 1;                  // largest backward key offset
+    static constexpr int XS = (PAD + kNmp + 1) / 2 * 2;           // state row stride
+    static constexpr int NCELL = N * N * N;
+    static_assert(Q <= kNmp - 1 && Q >= PAD && CL <= kMaxCluster, "cluster geometry");
+};
+
+template <int N>
+size_t cluster_vertex_smem() {
+    using G = ClusterGeom<N>;
+    return (6ull * G::XS + 65ull * kNmp + 2ull * (G::NCELL + 1)) * sizeof(double);
+}
+
+template <int N>
+__global__ void __launch_bounds__(kNmp, 1) cluster_vertex_kernel(ClArgs A) {
+    using G = ClusterGeom<N>;
+    constexpr int CL = G::CL, Q = G::Q, PAD = G::PAD, XS = G::XS, VW = G::VW, NV = G::NV;
+    constexpr int NTV = G::NCELL + 1;
+    const uint32_t rank = cluster_rank();
+    const int r = blockIdx.x / CL;
+    const BatchView& b = A.b;
+    const int64_t mo = b.mass_off[r], so = b.spring_off[r];
+    const int nm = b.nmass[r];
+    const int a = threadIdx.x;
+    vx_summary* out = (A.out && rank == 0) ? A.out + r : nullptr;
+
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    double* X = reinterpret_cast<double*>(smem_raw);  // [6][XS]: keys lo - PAD .. lo + kNmp
+    double* F = X + 6 * XS;                            // [13*3][kNmp] force on the lower endpoint
+    double* PR = F + 39 * kNmp;                        // [13][kNmp] rest0 of backward slot (d, key)
+    double* PC = PR + 13 * kNmp;                       // [13][kNmp] damping coefficient
+    double* D = PC + 13 * kNmp;                        // [NTV] drive per voxel
+    double* SA = D + NTV;                              // [NTV] sign*amplitude
+    int* MAP = reinterpret_cast<int*>(F);              // prologue: key -> mass index (-1 absent)
+    double* SPH = F + (NV + 1) / 2 + 8;                // prologue: sin/cos(phase) staging
+    double* CPH = SPH + NTV;
+    __shared__ double s_maxsq[kNmp / 32];
+    __shared__ double s_cmax[kMaxCluster];
+    __shared__ uint32_t s_flag;
+
+    if (nm == 0) {  // uniform over the cluster: every CTA leaves, rank 0 reports
+        if (out && a == 0) {
+            for (int c = 0; c < 3; ++c) out->com_start[c] = out->com_end[c] = 0.0;
+            out->horizontal_displacement = 0.0;
+            out->max_speed = 0.0;
+            out->diverged = 0;
+            out->steps = 0;
+            out->spring_updates = 0;
+        }
+        return;
+    }
+    const int lo = static_cast<int>(rank) * Q;
+    const int g = lo + a;                               // vertex key of this thread
+    const bool in_range = a < Q && g < NV;
+    const bool has_next = static_cast<int>(rank) + 1 < CL;  // the next CTA owns keys (Q * CL >= NV)
+
+    // ---------------------------------------------------------- prologue
+    for (int v = a; v < NTV; v += kNmp) {
+        SA[v] = 0.0;
+        SPH[v] = 0.0;
+        CPH[v] = 1.0;
+    }
+    for (int k = a; k < NV; k += kNmp) MAP[k] = -1;
+    if (a == 0) s_flag = 0u;
+    __syncthreads();
+    for (int m = a; m < nm; m += kNmp) MAP[A.vkey[mo + m]] = m;
+    const int ns = b.nspring[r];
+    for (int s = a; s < ns; s += kNmp) {
+        const int v = A.act_vox[so + s];
+        if (v >= 0) {
+            SA[v] = A.sign[so + s] * A.amp[so + s];  // sign * amplitude (physics.hpp:153)
+            SPH[v] = b.sinph[so + s];
+            CPH[v] = b.cosph[so + s];
+        }
+    }
+    __syncthreads();
+    // state rows: halo keys [lo - PAD, lo) and own keys; absent -> far away
+    for (int li = a; li < PAD; li += kNmp) {
+        const int k = lo - PAD + li;
+        const int mm = k >= 0 ? MAP[k] : -1;
+        for (int c = 0; c < 3; ++c) {
+            X[c * XS + li] = mm >= 0 ? b.pos[c * b.M + mo + mm] : 1e3;
+            X[(3 + c) * XS + li] = mm >= 0 ? b.vel[c * b.M + mo + mm] : 0.0;
+        }
+    }
+    const int m = in_range ? MAP[g] : -1;
+    const bool live = m >= 0;
+    const bool push_halo = live && has_next && a >= Q - PAD;  // the next CTA's halo holds this key
+    double pk[13];
+    uint32_t pvox[7];
+    unsigned fmask = 0u, bmask = 0u;
+    double mg = 0.0, imdt = 0.0, gdmp = 0.0;
+    double x0 = 1e3, x1 = 1e3, x2 = 1e3, v0 = 0.0, v1 = 0.0, v2 = 0.0;
+#pragma unroll
+    for (int d = 0; d < 13; ++d) {
+        pk[d] = 0.0;
+        PR[d * kNmp + a] = 1.0;
+        PC[d * kNmp + a] = 0.0;
+    }
+#pragma unroll
+    for (int qv = 0; qv < 7; ++qv) pvox[qv] = static_cast<uint32_t>(G::NCELL) * 0x10001u;
+    if (live) {
+        x0 = b.pos[mo + m];
+        x1 = b.pos[b.M + mo + m];
+        x2 = b.pos[2 * b.M + mo + m];
+        v0 = b.vel[mo + m];
+        v1 = b.vel[b.M + mo + m];
+        v2 = b.vel[2 * b.M + mo + m];
+        const double mm = b.mass[mo + m];
+        mg = mm * A.sp.gravity;  // physics.hpp:226
+        imdt = A.sp.dt / mm;     // physics.hpp:249
+        gdmp = b.gdamp[mo + m];
+        const int32_t* inc_off = b.inc_off + mo + r;
+        const uint32_t* inc = b.inc + 2 * so;
+        for (int e = inc_off[m]; e < inc_off[m + 1]; ++e) {
+            const uint32_t iv = inc[e];
+            const int sp = static_cast<int>(iv >> 1);
+            const uint32_t ij = b.ij[so + sp];
+            const int other = (iv & 1u) ? static_cast<int>(ij & 0xFFFFu) : static_cast<int>(ij >> 16);
+            const int kb = A.vkey[mo + other];
+            const int dx = kb % VW - g % VW, dy = (kb / VW) % VW - (g / VW) % VW, dz = kb / (VW * VW) - g / (VW * VW);
+            const int L = 9 * dz + 3 * dy + dx;
+            const int dd = (L > 0 ? L : -L) - 1;
+#pragma unroll
+            for (int d = 0; d < 13; ++d) {
+                if (d == dd) {
+                    if (L < 0) {
+                        bmask |= 1u << d;
+                        pk[d] = b.k[so + sp];
+                        PR[d * kNmp + a] = b.rest0[so + sp];
+                        PC[d * kNmp + a] = b.c[so + sp];
+                        const int av = A.act_vox[so + sp];
+                        const uint32_t vv = static_cast<uint32_t>(av >= 0 ? av : G::NCELL);
+                        const int sh = 16 * (d & 1);
+                        pvox[d >> 1] = (pvox[d >> 1] & ~(0xFFFFu << sh)) | (vv << sh);
+                    } else {
+                        fmask |= 1u << d;
+                    }
+                }
+            }
+        }
+    }
+    __syncthreads();
+    double vsin[kVpt], vcos[kVpt];
+    {
+        const double2 drv = __ldg(A.drive);
+#pragma unroll
+        for (int j = 0; j < kVpt; ++j) {
+            const int v = a + j * kNmp;
+            vsin[j] = v < NTV ? SPH[v] : 0.0;
+            vcos[j] = v < NTV ? CPH[v] : 1.0;
+            if (v < NTV) D[v] = drv.x * vcos[j] + drv.y * vsin[j];
+        }
+    }
+    X[PAD + a] = x0;  // own rows (absent / out-of-range keys: far away, at rest)
+    X[XS + PAD + a] = x1;
+    X[2 * XS + PAD + a] = x2;
+    X[3 * XS + PAD + a] = v0;
+    X[4 * XS + PAD + a] = v1;
+    X[5 * XS + PAD + a] = v2;
+    const unsigned wmask = __reduce_or_sync(0xffffffffu, bmask);
+    double com_start[3] = {0.0, 0.0, 0.0};
+    if (out && a == 0) {  // center_of_mass (physics.hpp:266-278) of the initial state, in mass order
+        double c0 = 0.0, c1 = 0.0, c2 = 0.0, total = 0.0;
+        for (int q = 0; q < nm; ++q) {
+            const double w = b.mass[mo + q];
+            c0 += w * b.pos[mo + q];
+            c1 += w * b.pos[b.M + mo + q];
+            c2 += w * b.pos[2 * b.M + mo + q];
+            total += w;
+        }
+        if (total > 0.0) {
+            c0 /= total;
+            c1 /= total;
+            c2 /= total;
+        }
+        com_start[0] = c0;
+        com_start[1] = c1;
+        com_start[2] = c2;
+    }
+    const uint32_t f_prev = rank > 0 ? map_rank(smem_addr(F), rank - 1) : 0u;
+    const uint32_t x_next = has_next ? map_rank(smem_addr(X), rank + 1) : 0u;
+    const uint32_t flag_local = smem_addr(&s_flag);
+    cluster_barrier();  // every CTA initialised (MAP and staging in F are dead) before any remote store
+
+    const double dt = A.sp.dt;
+    const double plane_k = A.sp.plane_k, mu_s = A.sp.mu_s, mu_k = A.sp.mu_k;
+    const bool en_grav = A.sp.en_grav, en_contact = A.sp.en_contact;
+    double max_sq = 0.0;
+    int64_t steps = 0, ok_phase1 = 0;
+    int diverged = 0;
+    auto raise_flag = [&](uint32_t tag) {
+        for (int c = 0; c < CL; ++c) st_remote_u32(map_rank(flag_local, static_cast<uint32_t>(c)), tag);
+    };
+    const double* __restrict__ Xa = X + PAD + a;
+    for (int64_t kstep = 0; kstep < A.n_steps; ++kstep) {
+        const uint32_t tag1 = static_cast<uint32_t>(2 * kstep + 1), tag2 = tag1 + 1u;
+        int zero_len = 0;
+        double sx = 0.0, sy = 0.0, sz = 0.0;
+        if (wmask) {
+            constexpr int kChunk = 5;
+#pragma unroll
+            for (int c0 = 12; c0 >= 0; c0 -= kChunk) {
+                double ofx[kChunk], ofy[kChunk], ofz[kChunk];
+#pragma unroll
+                for (int qq = 0; qq < kChunk; ++qq) {
+                    const int d = c0 - qq;
+                    if (d < 0) break;
+                    const int off = key_off<VW>(d);
+                    const bool valid = (bmask >> d) & 1u;
+                    const int vox = static_cast<int>((pvox[d >> 1] >> (16 * (d & 1))) & 0xFFFFu);
+                    VX_DCHECK(vox < NTV);
+                    double dx = x0 - Xa[-off];
+                    double dy = x1 - Xa[XS - off];
+                    double dz = x2 - Xa[2 * XS - off];
+                    const double len2 = dx * dx + dy * dy + dz * dz;
+                    const double len = sqrt_rn_fast(len2);
+                    zero_len |= (valid && len2 < A.zero_len2) ? 1 : 0;
+                    const double r0 = PR[d * kNmp + a];
+                    const double rest = r0 + (SA[vox] * r0) * D[vox];
+                    const double inv_len = rcp_rn_fast(len);
+                    const double nx = dx * inv_len, ny = dy * inv_len, nz = dz * inv_len;
+                    const double rel = (v0 - Xa[3 * XS - off]) * nx + (v1 - Xa[4 * XS - off]) * ny +
+                                       (v2 - Xa[5 * XS - off]) * nz;
+                    const double mag = pk[d] * (len - rest) + PC[d * kNmp + a] * rel;
+                    ofx[qq] = mag * nx;
+                    ofy[qq] = mag * ny;
+                    ofz[qq] = mag * nz;
+                }
+#pragma unroll
+                for (int qq = 0; qq < kChunk; ++qq) {
+                    const int d = c0 - qq;
+                    if (d < 0) break;
+                    const int off = key_off<VW>(d);
+                    const bool valid = (bmask >> d) & 1u;
+                    if (valid) {
+                        sx -= ofx[qq];  // fx += (-1)*F == fx - F exactly
+                        sy -= ofy[qq];
+                        sz -= ofz[qq];
+                    }
+                    // lower endpoint key g - off: this CTA's slot a - off, or the
+                    // previous CTA's slot a - off + Q (predicated, no branch)
+                    const int li = a - off;
+                    const bool rem = li < 0;
+                    VX_DCHECK(!valid || (rem ? (rank > 0 && li + Q >= 0) : li < kNmp));
+                    if (valid && !rem) {
+                        F[(3 * d) * kNmp + li] = ofx[qq];
+                        F[(3 * d + 1) * kNmp + li] = ofy[qq];
+                        F[(3 * d + 2) * kNmp + li] = ofz[qq];
+                    }
+                    const uint32_t o = f_prev + 8u * static_cast<uint32_t>((3 * d) * kNmp + li + Q);
+                    st_remote_if(valid && rem, o, ofx[qq]);
+                    st_remote_if(valid && rem, o + 8u * kNmp, ofy[qq]);
+                    st_remote_if(valid && rem, o + 16u * kNmp, ofz[qq]);
+                }
+            }
+        }
+        ++steps;
+        if (zero_len) raise_flag(tag1);
+        cluster_barrier();
+        if (*reinterpret_cast<volatile uint32_t*>(&s_flag) == tag1) {
+            diverged = 1;
+            break;
+        }
+        ++ok_phase1;
+        int bad = 0;
+        if (live) {
+            double fx = sx, fy = sy, fz = sz;
+#pragma unroll
+            for (int d = 0; d < 13; ++d) {
+                if (fmask & (1u << d)) {
+                    fx += F[(3 * d) * kNmp + a];
+                    fy += F[(3 * d + 1) * kNmp + a];
+                    fz += F[(3 * d + 2) * kNmp + a];
+                }
+            }
+            if (en_grav) fz -= mg;
+            if (en_contact && x2 < 0.0) {
+                const double penetration = -x2;
+                double normal = plane_k * penetration - gdmp * v2;
+                if (normal < 0.0) normal = 0.0;
+                const double ft_norm = sqrt(fx * fx + fy * fy);
+                const double vt_norm = sqrt(v0 * v0 + v1 * v1);
+                if (vt_norm < kStickVelocity && ft_norm <= mu_s * normal) {
+                    fx = 0.0;
+                    fy = 0.0;
+                } else if (vt_norm > 0.0) {
+                    const double scale = mu_k * normal / vt_norm;
+                    fx -= scale * v0;
+                    fy -= scale * v1;
+                } else if (ft_norm > 0.0) {
+                    const double scale = mu_k * normal / ft_norm;
+                    fx -= scale * fx;
+                    fy -= scale * fy;
+                }
+                fz += normal;
+            }
+            v0 += fx * imdt;
+            v1 += fy * imdt;
+            v2 += fz * imdt;
+            x0 += v0 * dt;
+            x1 += v1 * dt;
+            x2 += v2 * dt;
+            X[PAD + a] = x0;
+            X[XS + PAD + a] = x1;
+            X[2 * XS + PAD + a] = x2;
+            X[3 * XS + PAD + a] = v0;
+            X[4 * XS + PAD + a] = v1;
+            X[5 * XS + PAD + a] = v2;
+            if (push_halo) {  // the next CTA's halo copy of this key: row a - Q + PAD there
+                const uint32_t o = x_next + 8u * static_cast<uint32_t>(a - Q + PAD);
+                st_remote(o, x0);
+                st_remote(o + 8u * XS, x1);
+                st_remote(o + 16u * XS, x2);
+                st_remote(o + 24u * XS, v0);
+                st_remote(o + 32u * XS, v1);
+                st_remote(o + 40u * XS, v2);
+            }
+            const double speed_sq = v0 * v0 + v1 * v1 + v2 * v2;
+            if (speed_sq > max_sq) max_sq = speed_sq;
+            if (!(fabs(x0) <= kDivergenceBound) || !(fabs(x1) <= kDivergenceBound) ||
+                !(fabs(x2) <= kDivergenceBound))
+                bad = 1;
+        }
+        if (kstep + 1 < A.n_steps) {
+            const double2 drv = __ldg(A.drive + kstep + 1);
+#pragma unroll
+            for (int j = 0; j < kVpt; ++j) {
+                const int v = a + j * kNmp;
+                if (v < NTV) D[v] = drv.x * vcos[j] + drv.y * vsin[j];
+            }
+        }
+        if (bad) raise_flag(tag2);
+        cluster_barrier();
+        if (*reinterpret_cast<volatile uint32_t*>(&s_flag) == tag2) {
+            diverged = 1;
+            break;
+        }
+    }
+
+    for (int o = 16; o > 0; o >>= 1) {
+        const double other = __shfl_xor_sync(0xffffffffu, max_sq, o);
+        if (other > max_sq) max_sq = other;
+    }
+    if ((a & 31) == 0) s_maxsq[a >> 5] = max_sq;
+    if (live) {
+        for (int c = 0; c < 3; ++c) {
+            A.xfinal[c * b.M + mo + m] = X[c * XS + PAD + a];
+            A.xfinal[(3 + c) * b.M + mo + m] = X[(3 + c) * XS + PAD + a];
+            if (A.write_back) {
+                b.pos[c * b.M + mo + m] = X[c * XS + PAD + a];
+                b.vel[c * b.M + mo + m] = X[(3 + c) * XS + PAD + a];
+            }
+        }
+    }
+    __syncthreads();
+    if (a == 0) {
+        double mx = 0.0;
+        for (int w = 0; w < kNmp / 32; ++w)
+            if (s_maxsq[w] > mx) mx = s_maxsq[w];
+        st_remote(map_rank(smem_addr(&s_cmax[rank]), 0u), mx);
+    }
+    __threadfence();
+    cluster_barrier();
+    if (out && a == 0) {
+        double mx = 0.0;
+        for (int c = 0; c < CL; ++c)
+            if (s_cmax[c] > mx) mx = s_cmax[c];
+        double c0 = 0.0, c1 = 0.0, c2 = 0.0, total = 0.0;
+        for (int q = 0; q < nm; ++q) {
+            const double w = b.mass[mo + q];
+            c0 += w * A.xfinal[mo + q];
+            c1 += w * A.xfinal[b.M + mo + q];
+            c2 += w * A.xfinal[2 * b.M + mo + q];
+            total += w;
+        }
+        if (total > 0.0) {
+            c0 /= total;
+            c1 /= total;
+            c2 /= total;
+        }
+        const double com_end[3] = {c0, c1, c2};
+        for (int c = 0; c < 3; ++c) {
+            out->com_start[c] = com_start[c];
+            out->com_end[c] = com_end[c];
+        }
+        const double dx = com_end[0] - com_start[0];
+        const double dy = com_end[1] - com_start[1];
+        out->horizontal_displacement = sqrt(dx * dx + dy * dy);
+        out->max_speed = sqrt(mx);
+        out->diverged = diverged;
+        out->steps = steps;
+        out->spring_updates = static_cast<uint64_t>(ok_phase1) * static_cast<uint64_t>(b.nspring[r]);
+    }
+}
+
 size_t cluster_smem(int ncell) { return (6ull * kXS + 65ull * kNmp + 2ull * (ncell + 1)) * sizeof(double); }
 
 int cluster_size_for(int nm_max) { return (nm_max + kNmp - 2) / (kNmp - 1); }
+
+// cubic grids 7..10 run the vertex-indexed cluster kernel (VX_CLUSTER=rank
+// forces the rank-indexed one, for A/B runs)
+int cluster_vertex_grid(const vx_batch* b) {
+    static const char* force = std::getenv("VX_CLUSTER");
+    if (force && std::string(force) == "rank") return 0;
+    if (b->lw != b->lh || b->lw != b->ld || b->lw < 7 || b->lw > 10) return 0;
+    return b->lw;
+}
 
 }  // namespace
 
@@ -505,8 +921,10 @@ bool cluster_applicable(vx_ctx* ctx, vx_batch* b) {
     const int ncell = b->lw * b->lh * b->ld;
     const int halo = (b->lw + 1) * (b->lh + 1) + (b->lw + 1) + 1;
     const int cl = cluster_size_for(b->nm_max);
-    if (cl < 2 || cl > kMaxCluster || halo > kH0 || ncell + 1 > kVpt * kNmp) return false;
-    if (cluster_smem(ncell) + 1024 > ctx->smem_optin) return false;
+    if (cluster_vertex_grid(b) == 0) {
+        if (cl < 2 || cl > kMaxCluster || halo > kH0 || ncell + 1 > kVpt * kNmp) return false;
+        if (cluster_smem(ncell) + 1024 > ctx->smem_optin) return false;
+    }
     if (ctx->cluster_ok < 0) {  // can a cluster of kMaxCluster such CTAs be co-scheduled?
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3(kMaxCluster);
@@ -550,23 +968,31 @@ vx_status integrate_cluster(vx_ctx* ctx, vx_batch* b, int64_t n_steps, bool writ
     A.zero_len2 = zero_len2;
     VX_TRY(ctx->cluster_state.alloc(6 * static_cast<size_t>(b->M)));
     A.xfinal = ctx->cluster_state.p;
-    const size_t smem = cluster_smem(A.ncell);
-    VX_CUDA(cudaFuncSetAttribute(cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(static_cast<unsigned>(b->n * A.cl));
-    cfg.blockDim = dim3(kNmp);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = ctx->stream;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = static_cast<unsigned>(A.cl);
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    VX_CUDA(cudaLaunchKernelEx(&cfg, cluster_kernel, A));
-    ctx->launches++;
-    return VX_OK;
+    auto launch = [&](auto kernel, int cl, size_t smem) -> vx_status {
+        VX_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(static_cast<unsigned>(b->n * cl));
+        cfg.blockDim = dim3(kNmp);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = ctx->stream;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = static_cast<unsigned>(cl);
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        VX_CUDA(cudaLaunchKernelEx(&cfg, kernel, A));
+        ctx->launches++;
+        return VX_OK;
+    };
+    switch (cluster_vertex_grid(b)) {
+        case 7: return launch(cluster_vertex_kernel<7>, ClusterGeom<7>::CL, cluster_vertex_smem<7>());
+        case 8: return launch(cluster_vertex_kernel<8>, ClusterGeom<8>::CL, cluster_vertex_smem<8>());
+        case 9: return launch(cluster_vertex_kernel<9>, ClusterGeom<9>::CL, cluster_vertex_smem<9>());
+        case 10: return launch(cluster_vertex_kernel<10>, ClusterGeom<10>::CL, cluster_vertex_smem<10>());
+        default: return launch(cluster_kernel, A.cl, cluster_smem(A.ncell));
+    }
 }
 
 }  // namespace vx

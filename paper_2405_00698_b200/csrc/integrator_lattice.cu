@@ -397,16 +397,6 @@ __global__ void __launch_bounds__(NMP, 1) lattice_kernel(LatArgs A) {
 // (like the ghost); the state rows carry PAD leading far-away entries so that
 // key - offset never underflows.  Masses are still processed in mass order
 // wherever order matters (centre of mass), via the key of each mass.
-constexpr int kOffDy(int d) {  // decomposition of forward direction d: L = d + 1 = 9dz + 3dy + dx
-    return ((d + 1) - 9 * ((d + 1) >= 5 ? 1 : 0) + 7) / 3 - 2;
-}
-constexpr int kOffDz(int d) { return (d + 1) >= 5 ? 1 : 0; }
-constexpr int kOffDx(int d) { return (d + 1) - 9 * kOffDz(d) - 3 * kOffDy(d); }
-template <int VW>
-constexpr int key_off(int d) {  // key offset of forward direction d on a VW x VW x VW vertex lattice
-    return kOffDz(d) * VW * VW + kOffDy(d) * VW + kOffDx(d);
-}
-
 template <int N>
 struct VertexGeom {
     static constexpr int VW = N + 1;
