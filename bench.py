@@ -296,7 +296,7 @@ def main():
     peak_tf = ctx.fp64_peak_tflops()
     roofline = {"bound": "fp64", "achieved": achieved_tf, "peak": peak_tf, "unit": "TFLOP/s",
                 "frac": (achieved_tf / peak_tf) if achieved_tf else None, "traffic": _ncu_traffic(),
-                "kernel": "lattice_kernel<352> (fused integrator K7-K9)", "kernel_ms_avg": avg_int_ms,
+                "kernel": "vertex_kernel<6> (fused integrator K7-K9, vertex-key-indexed)", "kernel_ms_avg": avg_int_ms,
                 "kernel_share_of_step": (int_ms / total_ms) if total_ms else None,
                 "peak_source": "measured DFMA throughput on this GPU (vx_fp64_peak; MEASURED_PEAKS.json has no "
                                "FP64 entry), 2 flop/DFMA",
