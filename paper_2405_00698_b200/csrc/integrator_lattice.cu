@@ -627,11 +627,11 @@ __global__ void __launch_bounds__(VertexGeom<N>::NT, 1) vertex_kernel(LatArgs A)
                 }
             }
         };
-        using I3 = std::integral_constant<int, 3>;
+        // chunks 12..9 | 8..4 | 3..0 measured best for this kernel (profiles/README.md)
         using I4 = std::integral_constant<int, 4>;
-        if (wmask & 0x1C00u) chunk(std::integral_constant<int, 12>{}, I3{});
-        if (wmask & 0x0380u) chunk(std::integral_constant<int, 9>{}, I3{});
-        if (wmask & 0x0070u) chunk(std::integral_constant<int, 6>{}, I3{});
+        using I5 = std::integral_constant<int, 5>;
+        if (wmask & 0x1E00u) chunk(std::integral_constant<int, 12>{}, I4{});
+        if (wmask & 0x01F0u) chunk(std::integral_constant<int, 8>{}, I5{});
         if (wmask & 0x000Fu) chunk(std::integral_constant<int, 3>{}, I4{});
         ++steps;
         if (__syncthreads_or(zero_len)) {  // step() returns diverged; masses untouched
