@@ -47,3 +47,25 @@ def test_specialised_integrators_nondefault(vx, ctx, orc, n, variant):
         np.testing.assert_array_equal(got.robot(r)["pos"], ref.pos, err_msg=f"{variant} grid {n} robot {r}")
         np.testing.assert_array_equal(got.robot(r)["vel"], ref.vel, err_msg=f"{variant} grid {n} robot {r}")
         assert out[r].spring_updates == upd and out[r].max_speed == np.sqrt(msq)
+
+
+@pytest.mark.parametrize("n,steps", [(6, 5000), (10, 5000), (20, 1000)])
+def test_full_horizon_bit_exact(vx, ctx, orc, n, steps):
+    """The benchmark horizon (5000 steps; 1000 for 20^3 to keep the CPU
+    reference quick): a decoded robot stays bit-identical to the reference's
+    step() the whole way on every specialised kernel."""
+    rng = np.random.default_rng(1000 + n)
+    g = orc.sample_genome(32, [64, 64], int(rng.integers(0, 2 ** 62)))
+    mats, wts = vx.decode(g[0][None], g[1][None], vx.Arch.make(), n, n, n, ctx)
+    body = orc.largest_component(mats[0], n, n, n)
+    batch = vx.build_mass_spring(body[None], wts, n, n, n, ctx=ctx)
+    s = orc.build(body, wts[0], n, n, n)
+    ws = orc.workspace(s)
+    batch.override_phase(ws["sin_phase"], ws["cos_phase"])
+    out = batch.step(vx.SimConfig(), 0, steps)[0]
+    assert ctx.last_integrator == KERNEL[n]
+    ref, ok, called, upd, msq = orc.step(s, vx.SimConfig().as_array(), 0, steps)
+    got = batch.download()
+    np.testing.assert_array_equal(got.pos, ref.pos)
+    np.testing.assert_array_equal(got.vel, ref.vel)
+    assert out.spring_updates == upd and out.max_speed == np.sqrt(msq)
