@@ -1,6 +1,9 @@
 #!/usr/bin/env python
 """bench.py — spring-mass updates/s of the voxevo hot path on B200.
 
+(--workload config3 / config5 run BASELINE configs 3 / 5 under the same
+contract: one generation of P=4096 10^3 / P=1024 20^3 robots per step.)
+
 Workload (BASELINE.json configs[1], "config 2"): population 256 of 6x6x6 voxel
 robots per GPU, ONE generation = decode (Fourier encoding + MLP) -> largest
 component -> mass-spring assembly -> 5000-step fused integrator (dt 1e-5) ->
@@ -36,6 +39,20 @@ sys.path.insert(0, ROOT)
 P_PER_GPU = 256
 GRID = 6
 SIM_STEPS = 5000
+# --workload: the default is config 2 (BASELINE.json configs[1], the driver's
+# line); configs 3 and 5 run one generation of their population per step
+WORKLOADS = {
+    "config2": dict(P=256, grid=6, kernel="vertex_kernel<6> (fused integrator K7-K9, vertex-key-indexed)",
+                    desc="config 2: P=256 6x6x6 per GPU, 1 generation (decode + 5000-step fitness + sort/stats/"
+                         "diversity + breed)"),
+    "config3": dict(P=4096, grid=10, kernel="cluster_vertex_kernel<10> (4-CTA thread-block cluster per robot)",
+                    desc="config 3: P=4096 10x10x10 per GPU, 1 of the 50 generations per step (decode + "
+                         "5000-step fitness + sort/stats/diversity + breed)"),
+    "config5": dict(P=1024, grid=20, kernel="stream_vertex_kernel<20> (streaming integrator)",
+                    desc="config 5: P=1024 20x20x20 per GPU, 1 generation (decode + 5000-step fitness + sort/"
+                         "stats/diversity + breed)"),
+}
+CPU_SAMPLE_MAX = 256  # robots in the bounded cpu_baseline sample
 DT = 1e-5
 SEED = 42
 FLOPS_PER_UPDATE = 48  # 48 FP64 flop (+1 sqrt +1 div) per spring update
@@ -175,12 +192,12 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": value, "unit": "spring_updates/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / len(times),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "config 2: P=256 6x6x6, 1 generation (decode + 5000-step fitness + breed)",
-                   "population": P, "grid": [GRID] * 3, "sim_steps": SIM_STEPS, "dt": DT, "seed": SEED},
+        "config": {"workload": args.desc, "population": P, "grid": [GRID] * 3, "sim_steps": SIM_STEPS, "dt": DT,
+                   "seed": SEED},
         "generations_per_s": len(times) / total,
         "cpu_baseline": {"value": value, "unit": "spring_updates/s", "cores": threads, "kind": "reference",
-                         "sample": "full config-2 evolve_generation (P=256, 6^3, 5000 steps), reference headers "
-                                   "compiled -O2 no -march, std::thread parallel_for"},
+                         "sample": f"full evolve_generation (P={P}, {GRID}^3, {SIM_STEPS} steps), reference "
+                                   "headers compiled -O2 no -march, std::thread parallel_for"},
         "e2e": {"value": value, "unit": "spring_updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
@@ -194,7 +211,12 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no baselines, no clocks)")
+    ap.add_argument("--workload", default="config2", choices=sorted(WORKLOADS))
     args = ap.parse_args()
+    global P_PER_GPU, GRID
+    W = WORKLOADS[args.workload]
+    P_PER_GPU, GRID = W["P"], W["grid"]
+    args.kernel, args.desc = W["kernel"], W["desc"]
     if args.impl == "reference":
         run_reference(args)
         return
@@ -294,15 +316,17 @@ def main():
     avg_int_ms = int_ms / max(1, int_n)
     achieved_tf = FLOPS_PER_UPDATE * local_upd / (avg_int_ms * 1e-3) / 1e12 if int_n else None
     peak_tf = ctx.fp64_peak_tflops()
+    default = args.workload == "config2"  # the committed ncu capture is of the config-2 kernel
     roofline = {"bound": "fp64", "achieved": achieved_tf, "peak": peak_tf, "unit": "TFLOP/s",
-                "frac": (achieved_tf / peak_tf) if achieved_tf else None, "traffic": _ncu_traffic(),
-                "kernel": "vertex_kernel<6> (fused integrator K7-K9, vertex-key-indexed)", "kernel_ms_avg": avg_int_ms,
+                "frac": (achieved_tf / peak_tf) if achieved_tf else None,
+                "traffic": _ncu_traffic() if default else None,
+                "kernel": args.kernel, "kernel_ms_avg": avg_int_ms,
                 "kernel_share_of_step": (int_ms / total_ms) if total_ms else None,
                 "peak_source": "measured DFMA throughput on this GPU (vx_fp64_peak; MEASURED_PEAKS.json has no "
                                "FP64 entry), 2 flop/DFMA",
                 "algorithmic": f"{FLOPS_PER_UPDATE} FP64 flop + 1 sqrt + 1 div per spring update x "
                                f"{local_upd} updates per launch",
-                "fp64_pipe_busy_ncu": _ncu_field("fp64_pipe_pct"),
+                "fp64_pipe_busy_ncu": _ncu_field("fp64_pipe_pct") if default else None,
                 "note": "parity mode forbids FMA contraction and IEEE sqrt/1/x cost ~15 FP64 instructions for 2 "
                         "counted flop, so the flop fraction is structurally capped near 40%; fp64_pipe_busy_ncu is "
                         "the FP64-pipe utilisation of the same kernel from the committed ncu capture"}
@@ -310,13 +334,14 @@ def main():
     cpu = None
     if world == 1 and not args.no_cpu_baseline and not args.profile:
         pop = st.population()  # after the last step: elites keep grids -> re-decode for the sample
-        mats, wts = vx.decode(init_params.cpu().numpy(), init_bmat.cpu().numpy(), st.config.arch, GRID, GRID, GRID,
-                              ctx)
+        ns = min(P, CPU_SAMPLE_MAX if GRID <= 6 else 32)  # bounded: ~2-20 s of host work
+        mats, wts = vx.decode(init_params[:ns].cpu().numpy(), init_bmat[:ns].cpu().numpy(), st.config.arch, GRID,
+                              GRID, GRID, ctx)
         upd, meta = cpu_baseline_sample(mats, wts)
         cpu = {"value": (upd / meta["secs"]) if upd else None, "unit": "spring_updates/s", "cores": meta["cores"],
                "kind": meta["kind"],
-               "sample": f"evaluate_fitness over this config's {mats.shape[0]} decoded 6^3 robots x {SIM_STEPS} "
-                         f"steps ({upd} updates) via the reference's parallel_for, {meta['secs']:.2f} s"}
+               "sample": f"evaluate_fitness over {mats.shape[0]} of this config's decoded {GRID}^3 robots x "
+                         f"{SIM_STEPS} steps ({upd} updates) via the reference's parallel_for, {meta['secs']:.2f} s"}
         del pop
     h2d = P * (np_ + nb) * 8
     d2h = P * 8 + P * 8 + 3 * 8 + 8 + 4
@@ -324,8 +349,7 @@ def main():
         "metric": METRIC, "value": value, "unit": "spring_updates/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "config 2: P=256 6x6x6 per GPU, 1 generation (decode + 5000-step fitness + sort/"
-                               "stats/diversity + breed)", "population": P, "grid": [GRID] * 3,
+        "config": {"workload": args.desc, "population": P, "grid": [GRID] * 3,
                    "sim_steps": SIM_STEPS, "dt": DT, "seed": SEED, "l2": "flushed (256 MiB write) between steps",
                    "parallelism": f"population shards x{world}"},
         "generations_per_s": args.steps / (total_ms * 1e-3),
