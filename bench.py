@@ -48,7 +48,7 @@ WORKLOADS = {
     "config3": dict(P=4096, grid=10, kernel="cluster_vertex_kernel<10> (4-CTA thread-block cluster per robot)",
                     desc="config 3: P=4096 10x10x10 per GPU, 1 of the 50 generations per step (decode + "
                          "5000-step fitness + sort/stats/diversity + breed)"),
-    "config5": dict(P=1024, grid=20, kernel="stream_vertex_kernel<20> (streaming integrator)",
+    "config5": dict(P=1024, grid=20, kernel="stream_sym_kernel<20> (symmetric streaming integrator)",
                     desc="config 5: P=1024 20x20x20 per GPU, 1 generation (decode + 5000-step fitness + sort/"
                          "stats/diversity + breed)"),
 }
