@@ -436,405 +436,6 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(StreamArgs A)
 }
 
 // ---------------------------------------------------------------------------
-// stream_vertex_kernel<N>: the streaming integrator for N^3 grids indexed by
-// LATTICE VERTEX KEY (as vertex_kernel / cluster_vertex_kernel): every
-// neighbour is at a compile-time key offset, so the per-slot neighbour index
-// disappears (the actuating voxel is a u16), and a warp's neighbour gathers,
-// force-slot stores and parameter loads are all consecutive (fewer L2 sectors
-// per request than the rank-indexed gathers of sparse robots).  Absent
-// vertices are parked far away; the state rows carry PAD far entries below
-// key 0.
-template <int N>
-struct StreamGeom {
-    static constexpr int VW = N + 1;
-    static constexpr int NV = VW * VW * VW;
-    static constexpr int T = kStreamThreads;
-    static constexpr int MPT = (NV + T - 1) / T;     // keys per thread
-    static constexpr int NVP = MPT * T;              // padded keys
-    static constexpr int PAD = VW * VW + VW + 1;
-    static constexpr int XS = PAD + NVP;             // state row stride
-    static constexpr int NCELL = N * N * N;
-};
-
-struct SVLayout {
-    size_t per_robot, k, r0, vox, f, s, x, mc, mask, cph, sph, sa;
-};
-
-template <int N>
-SVLayout sv_layout() {
-    using G = StreamGeom<N>;
-    SVLayout L{};
-    size_t o = 0;
-    auto take = [&](size_t bytes) {
-        const size_t at = o;
-        o += (bytes + 255) / 256 * 256;
-        return at;
-    };
-    const size_t n = G::NVP;
-    L.k = take(13 * n * 8);
-    L.r0 = take(13 * n * 8);
-    L.vox = take(13 * n * 2);
-    L.f = take(39 * n * 8);
-    L.s = take(3 * n * 8);
-    L.x = take(6ull * G::XS * 8);
-    L.mc = take(3 * n * 8);
-    L.mask = take(n * 4);
-    L.cph = take((G::NCELL + 1) * 8ull);
-    L.sph = take((G::NCELL + 1) * 8ull);
-    L.sa = take((G::NCELL + 1) * 8ull);
-    L.per_robot = o;
-    return L;
-}
-
-struct SVArgs {
-    BatchView b;
-    const int32_t* vkey;
-    const int16_t* act_vox;
-    const double* sign;
-    const double* amp;
-    const double2* drive;
-    SimParams sp;
-    int64_t n_steps;
-    int write_back;
-    vx_summary* out;
-    unsigned char* scratch;
-    SVLayout L;
-    double zero_len2;
-    double zeta2, mu;
-};
-
-template <int N>
-__global__ void __launch_bounds__(1024) stream_vertex_prep_kernel(SVArgs A) {
-    using G = StreamGeom<N>;
-    constexpr int NVP = G::NVP, XS = G::XS, PAD = G::PAD, VW = G::VW;
-    const int r = blockIdx.x;
-    const BatchView& b = A.b;
-    const SVLayout& L = A.L;
-    unsigned char* base = A.scratch + static_cast<size_t>(r) * L.per_robot;
-    double* K = at<double>(base, L.k);
-    double* R0 = at<double>(base, L.r0);
-    uint16_t* VOX = at<uint16_t>(base, L.vox);
-    double* X = at<double>(base, L.x);
-    double* MC = at<double>(base, L.mc);
-    uint32_t* MASK = at<uint32_t>(base, L.mask);
-    double* CPH = at<double>(base, L.cph);
-    double* SPH = at<double>(base, L.sph);
-    double* SAG = at<double>(base, L.sa);
-    const int64_t mo = b.mass_off[r], so = b.spring_off[r];
-    const int nm = b.nmass[r], ns = b.nspring[r];
-    for (int v = threadIdx.x; v <= G::NCELL; v += blockDim.x) {
-        CPH[v] = 1.0;
-        SPH[v] = 0.0;
-        SAG[v] = 0.0;
-    }
-    for (int k = threadIdx.x; k < NVP; k += blockDim.x) {
-        for (int d = 0; d < 13; ++d) {
-            K[d * NVP + k] = 1.0;  // missing spring: any normal value (its result is discarded)
-            R0[d * NVP + k] = 1.0;
-            VOX[d * NVP + k] = static_cast<uint16_t>(G::NCELL);
-        }
-        MASK[k] = 0u;
-        MC[k] = MC[NVP + k] = MC[2 * NVP + k] = 0.0;
-    }
-    for (int q = threadIdx.x; q < XS; q += blockDim.x)  // every vertex (and the padding) far away, at rest
-        for (int c = 0; c < 6; ++c) X[c * XS + q] = c < 3 ? 1e3 : 0.0;
-    __syncthreads();
-    for (int s = threadIdx.x; s < ns; s += blockDim.x) {
-        const int v = A.act_vox[so + s];
-        if (v >= 0) {
-            CPH[v] = b.cosph[so + s];
-            SPH[v] = b.sinph[so + s];
-            SAG[v] = A.sign[so + s] * A.amp[so + s];  // sign * amplitude (physics.hpp:153)
-        }
-    }
-    for (int m = threadIdx.x; m < nm; m += blockDim.x) {
-        const int key = A.vkey[mo + m];
-        for (int c = 0; c < 3; ++c) {
-            X[c * XS + PAD + key] = b.pos[c * b.M + mo + m];
-            X[(3 + c) * XS + PAD + key] = b.vel[c * b.M + mo + m];
-        }
-        const double mm = b.mass[mo + m];
-        MC[key] = mm * A.sp.gravity;      // physics.hpp:226
-        MC[NVP + key] = A.sp.dt / mm;     // physics.hpp:249
-        MC[2 * NVP + key] = b.gdamp[mo + m];
-        const int32_t* inc_off = b.inc_off + mo + r;
-        const uint32_t* inc = b.inc + 2 * so;
-        unsigned fmask = 0u, bmask = 0u;
-        for (int e = inc_off[m]; e < inc_off[m + 1]; ++e) {
-            const uint32_t iv = inc[e];
-            const int sp = static_cast<int>(iv >> 1);
-            const uint32_t ij = b.ij[so + sp];
-            const int other = (iv & 1u) ? static_cast<int>(ij & 0xFFFFu) : static_cast<int>(ij >> 16);
-            const int kb = A.vkey[mo + other];
-            const int dx = kb % VW - key % VW, dy = (kb / VW) % VW - (key / VW) % VW,
-                      dz = kb / (VW * VW) - key / (VW * VW);
-            const int Lc = 9 * dz + 3 * dy + dx;
-            const int d = (Lc > 0 ? Lc : -Lc) - 1;
-            if (Lc < 0) {
-                bmask |= 1u << d;
-                K[d * NVP + key] = b.k[so + sp];
-                R0[d * NVP + key] = b.rest0[so + sp];
-                const int av = A.act_vox[so + sp];
-                VOX[d * NVP + key] = static_cast<uint16_t>(av >= 0 ? av : G::NCELL);
-            } else {
-                fmask |= 1u << d;
-            }
-        }
-        MASK[key] = bmask | (fmask << 13) | (1u << 26);  // bit 26: the vertex is a mass
-    }
-}
-
-template <int N>
-__global__ void __launch_bounds__(kStreamThreads, 1) stream_vertex_kernel(SVArgs A) {
-    using G = StreamGeom<N>;
-    constexpr int NVP = G::NVP, XS = G::XS, PAD = G::PAD, VW = G::VW, T = G::T, MPT = G::MPT, NV = G::NV;
-    constexpr int NT = G::NCELL + 1;
-    const int r = blockIdx.x;
-    const BatchView& b = A.b;
-    const SVLayout& L = A.L;
-    const int t = threadIdx.x;
-    unsigned char* base = A.scratch + static_cast<size_t>(r) * L.per_robot;
-    const double* __restrict__ K = at<double>(base, L.k);
-    const double* __restrict__ R0 = at<double>(base, L.r0);
-    const uint16_t* __restrict__ VOX = at<uint16_t>(base, L.vox);
-    const double* __restrict__ MC = at<double>(base, L.mc);
-    const uint32_t* __restrict__ MASK = at<uint32_t>(base, L.mask);
-    const double* SAG = at<double>(base, L.sa);
-    const double* CPH = at<double>(base, L.cph);
-    const double* SPH = at<double>(base, L.sph);
-    double* F = at<double>(base, L.f);
-    double* S = at<double>(base, L.s);
-    double* X = at<double>(base, L.x);
-    const int64_t mo = b.mass_off[r];
-    const int nm = b.nmass[r];
-    vx_summary* out = A.out ? A.out + r : nullptr;
-
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    double* D = reinterpret_cast<double*>(smem_raw);  // [NT] drive per voxel
-    double* SA = D + NT;                               // [NT] sign*amplitude per voxel
-    __shared__ double s_maxsq[32];
-
-    if (nm == 0) {
-        if (out && t == 0) {
-            for (int c = 0; c < 3; ++c) out->com_start[c] = out->com_end[c] = 0.0;
-            out->horizontal_displacement = 0.0;
-            out->max_speed = 0.0;
-            out->diverged = 0;
-            out->steps = 0;
-            out->spring_updates = 0;
-        }
-        return;
-    }
-    {
-        const double2 drv = __ldg(A.drive);
-        for (int v = t; v < NT; v += T) {
-            D[v] = drv.x * CPH[v] + drv.y * SPH[v];
-            SA[v] = SAG[v];
-        }
-    }
-    __syncthreads();
-    auto com = [&](double* o3) {  // center_of_mass (physics.hpp:266-278) in mass order
-        double c0 = 0.0, c1 = 0.0, c2 = 0.0, total = 0.0;
-        for (int q = 0; q < nm; ++q) {
-            const double w = b.mass[mo + q];
-            const int k = PAD + A.vkey[mo + q];
-            c0 += w * X[k];
-            c1 += w * X[XS + k];
-            c2 += w * X[2 * XS + k];
-            total += w;
-        }
-        if (total > 0.0) {
-            c0 /= total;
-            c1 /= total;
-            c2 /= total;
-        }
-        o3[0] = c0;
-        o3[1] = c1;
-        o3[2] = c2;
-    };
-    double com_start[3];
-    if (out && t == 0) com(com_start);
-
-    const double dt = A.sp.dt;
-    const double plane_k = A.sp.plane_k, mu_s = A.sp.mu_s, mu_k = A.sp.mu_k;
-    double max_sq = 0.0;
-    int64_t steps = 0, ok_phase1 = 0;
-    int diverged = 0;
-    for (int64_t kstep = 0; kstep < A.n_steps; ++kstep) {
-        // ---- phase 1: backward springs of every owned vertex (d = 12..0)
-        int zero_len = 0;
-        for (int j = 0; j < MPT; ++j) {
-            const int key = t + j * T;
-            const unsigned msk = key < NV ? MASK[key] : 0u;
-            const unsigned bmask = msk & 0x1FFFu;
-            if (__all_sync(0xffffffffu, bmask == 0u)) continue;  // absent / spring-less warp
-            const double* Xk = X + PAD + key;
-            const double x0 = Xk[0], x1 = Xk[XS], x2 = Xk[2 * XS];
-            const double v0 = Xk[3 * XS], v1 = Xk[4 * XS], v2 = Xk[5 * XS];
-            double sx = 0.0, sy = 0.0, sz = 0.0;
-#pragma unroll
-            for (int c0 = 12; c0 >= 0; c0 -= kStreamChunk) {
-                double ofx[kStreamChunk], ofy[kStreamChunk], ofz[kStreamChunk];
-#pragma unroll
-                for (int q = 0; q < kStreamChunk; ++q) {
-                    const int d = c0 - q;
-                    if (d < 0) break;
-                    const int off = key_off<VW>(d);
-                    const bool valid = (bmask >> d) & 1u;
-                    const int vox = VOX[d * NVP + key];
-                    VX_DCHECK(vox < NT);
-                    const double dx = x0 - Xk[-off];
-                    const double dy = x1 - Xk[XS - off];
-                    const double dz = x2 - Xk[2 * XS - off];
-                    const double len2 = dx * dx + dy * dy + dz * dz;
-                    const double len = sqrt_rn_fast(len2);
-                    zero_len |= (valid && len2 < A.zero_len2) ? 1 : 0;
-                    const double r0 = R0[d * NVP + key];
-                    const double rest = r0 + (SA[vox] * r0) * D[vox];
-                    const double inv_len = rcp_rn_fast(len);
-                    const double nx = dx * inv_len, ny = dy * inv_len, nz = dz * inv_len;
-                    const double rel = (v0 - Xk[3 * XS - off]) * nx + (v1 - Xk[4 * XS - off]) * ny +
-                                       (v2 - Xk[5 * XS - off]) * nz;
-                    // damping_coefficient (physics.hpp:66-71) recomputed (uniform masses)
-                    const double kk = K[d * NVP + key];
-                    const double cc = A.zeta2 * sqrt_rn_fast(kk * A.mu);
-                    const double mag = kk * (len - rest) + cc * rel;
-                    ofx[q] = mag * nx;
-                    ofy[q] = mag * ny;
-                    ofz[q] = mag * nz;
-                }
-#pragma unroll
-                for (int q = 0; q < kStreamChunk; ++q) {
-                    const int d = c0 - q;
-                    if (d < 0) break;
-                    const int off = key_off<VW>(d);
-                    if ((bmask >> d) & 1u) {
-                        sx -= ofx[q];
-                        sy -= ofy[q];
-                        sz -= ofz[q];
-                        VX_DCHECK(key - off >= 0);
-                        F[(3 * d) * NVP + key - off] = ofx[q];  // slot of the LOWER endpoint
-                        F[(3 * d + 1) * NVP + key - off] = ofy[q];
-                        F[(3 * d + 2) * NVP + key - off] = ofz[q];
-                    }
-                }
-            }
-            S[key] = sx;
-            S[NVP + key] = sy;
-            S[2 * NVP + key] = sz;
-        }
-        ++steps;
-        if (__syncthreads_or(zero_len)) {
-            diverged = 1;
-            break;
-        }
-        ++ok_phase1;
-        // ---- phase 2: forward terms d = 0..12, then gravity / contact / integrate
-        int bad = 0;
-        for (int j = 0; j < MPT; ++j) {
-            const int key = t + j * T;
-            const unsigned msk = key < NV ? MASK[key] : 0u;
-            if (!(msk >> 26)) continue;  // not a mass
-            const unsigned fmask = (msk >> 13) & 0x1FFFu;
-            double fx = (msk & 0x1FFFu) ? S[key] : 0.0, fy = (msk & 0x1FFFu) ? S[NVP + key] : 0.0,
-                   fz = (msk & 0x1FFFu) ? S[2 * NVP + key] : 0.0;
-#pragma unroll
-            for (int d = 0; d < 13; ++d) {
-                if (fmask & (1u << d)) {
-                    fx += F[(3 * d) * NVP + key];
-                    fy += F[(3 * d + 1) * NVP + key];
-                    fz += F[(3 * d + 2) * NVP + key];
-                }
-            }
-            double* Xk = X + PAD + key;
-            double px = Xk[0], py = Xk[XS], pz = Xk[2 * XS];
-            double vx = Xk[3 * XS], vy = Xk[4 * XS], vz = Xk[5 * XS];
-            if (A.sp.en_grav) fz -= MC[key];
-            if (A.sp.en_contact && pz < 0.0) {
-                const double penetration = -pz;
-                double normal = plane_k * penetration - MC[2 * NVP + key] * vz;
-                if (normal < 0.0) normal = 0.0;
-                const double ft_norm = sqrt(fx * fx + fy * fy);
-                const double vt_norm = sqrt(vx * vx + vy * vy);
-                if (vt_norm < kStickVelocity && ft_norm <= mu_s * normal) {
-                    fx = 0.0;
-                    fy = 0.0;
-                } else if (vt_norm > 0.0) {
-                    const double scale = mu_k * normal / vt_norm;
-                    fx -= scale * vx;
-                    fy -= scale * vy;
-                } else if (ft_norm > 0.0) {
-                    const double scale = mu_k * normal / ft_norm;
-                    fx -= scale * fx;
-                    fy -= scale * fy;
-                }
-                fz += normal;
-            }
-            const double imdt = MC[NVP + key];
-            vx += fx * imdt;
-            vy += fy * imdt;
-            vz += fz * imdt;
-            px += vx * dt;
-            py += vy * dt;
-            pz += vz * dt;
-            Xk[0] = px;
-            Xk[XS] = py;
-            Xk[2 * XS] = pz;
-            Xk[3 * XS] = vx;
-            Xk[4 * XS] = vy;
-            Xk[5 * XS] = vz;
-            const double speed_sq = vx * vx + vy * vy + vz * vz;
-            if (speed_sq > max_sq) max_sq = speed_sq;
-            if (!(fabs(px) <= kDivergenceBound) || !(fabs(py) <= kDivergenceBound) ||
-                !(fabs(pz) <= kDivergenceBound))
-                bad = 1;
-        }
-        if (kstep + 1 < A.n_steps) {
-            const double2 drv = __ldg(A.drive + kstep + 1);
-            for (int v = t; v < NT; v += T) D[v] = drv.x * CPH[v] + drv.y * SPH[v];
-        }
-        if (__syncthreads_or(bad)) {
-            diverged = 1;
-            break;
-        }
-    }
-
-    for (int o = 16; o > 0; o >>= 1) {
-        const double other = __shfl_xor_sync(0xffffffffu, max_sq, o);
-        if (other > max_sq) max_sq = other;
-    }
-    if ((t & 31) == 0) s_maxsq[t >> 5] = max_sq;
-    __syncthreads();
-    if (A.write_back) {
-        for (int q = t; q < nm; q += T) {
-            const int k = PAD + A.vkey[mo + q];
-            for (int c = 0; c < 3; ++c) {
-                b.pos[c * b.M + mo + q] = X[c * XS + k];
-                b.vel[c * b.M + mo + q] = X[(3 + c) * XS + k];
-            }
-        }
-    }
-    if (t == 0 && out) {
-        double m = 0.0;
-        for (int w = 0; w < T / 32; ++w)
-            if (s_maxsq[w] > m) m = s_maxsq[w];
-        double com_end[3];
-        com(com_end);
-        for (int c = 0; c < 3; ++c) {
-            out->com_start[c] = com_start[c];
-            out->com_end[c] = com_end[c];
-        }
-        const double dx = com_end[0] - com_start[0];
-        const double dy = com_end[1] - com_start[1];
-        out->horizontal_displacement = sqrt(dx * dx + dy * dy);
-        out->max_speed = sqrt(m);
-        out->diverged = diverged;
-        out->steps = steps;
-        out->spring_updates = static_cast<uint64_t>(ok_phase1) * static_cast<uint64_t>(b.nspring[r]);
-    }
-}
-
-// ---------------------------------------------------------------------------
 // stream_sym_kernel<N>: SYMMETRIC vertex-indexed streaming integrator — each
 // mass evaluates all of its springs itself in the reference's ascending
 // spring-index order (backward d = 12..0: fx -= F_i(neighbour, key); forward
@@ -1272,37 +873,6 @@ vx_status launch_stream_sym(vx_ctx* ctx, vx_batch* b, const StreamArgs& S) {
     return VX_OK;
 }
 
-template <int N>
-vx_status launch_stream_vertex(vx_ctx* ctx, vx_batch* b, const StreamArgs& S) {
-    SVArgs A{};
-    A.b = S.b;
-    A.vkey = S.vkey;
-    A.act_vox = S.act_vox;
-    A.sign = S.sign;
-    A.amp = S.amp;
-    A.drive = S.drive;
-    A.sp = S.sp;
-    A.n_steps = S.n_steps;
-    A.write_back = S.write_back;
-    A.out = S.out;
-    A.zero_len2 = S.zero_len2;
-    A.zeta2 = S.zeta2;
-    A.mu = S.mu;
-    A.L = sv_layout<N>();
-    VX_TRY(ctx->stream_scratch.alloc(A.L.per_robot * static_cast<size_t>(b->n)));
-    A.scratch = ctx->stream_scratch.p;
-    stream_vertex_prep_kernel<N><<<b->n, 1024, 0, ctx->stream>>>(A);
-    ctx->launches++;
-    VX_CUDA(cudaGetLastError());
-    const size_t smem = 2ull * (StreamGeom<N>::NCELL + 1) * sizeof(double);
-    VX_CUDA(cudaFuncSetAttribute(stream_vertex_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(smem)));
-    stream_vertex_kernel<N><<<b->n, kStreamThreads, smem, ctx->stream>>>(A);
-    ctx->launches++;
-    VX_CUDA(cudaGetLastError());
-    return VX_OK;
-}
-
 }  // namespace
 
 bool stream_applicable(vx_ctx* ctx, vx_batch* b) {
@@ -1332,13 +902,11 @@ vx_status integrate_stream(vx_ctx* ctx, vx_batch* b, int64_t n_steps, bool write
     A.zero_len2 = zero_len2;
     A.zeta2 = b->uniform_zeta * 2.0;
     A.mu = b->uniform_mass * b->uniform_mass / (b->uniform_mass + b->uniform_mass);
-    {  // 20^3 grids: the symmetric vertex-indexed kernel (measured 5.0e10 vs 3.8e10 for the
-       // force-slot vertex kernel); VX_STREAM=slots / rank select the others for A/B runs
+    {  // 20^3 grids: the symmetric vertex-indexed kernel (measured 5.0e10 vs 3.7e10 for the
+       // force-slot rank kernel below); VX_STREAM=rank forces the latter for A/B runs
         static const char* force = std::getenv("VX_STREAM");
-        const std::string f = force ? force : "";
-        const bool cube20 = b->lw == 20 && b->lh == 20 && b->ld == 20;
-        if (cube20 && f.empty()) return launch_stream_sym<20>(ctx, b, A);
-        if (cube20 && f == "slots") return launch_stream_vertex<20>(ctx, b, A);
+        const bool rank_only = force && std::string(force) == "rank";
+        if (!rank_only && b->lw == 20 && b->lh == 20 && b->ld == 20) return launch_stream_sym<20>(ctx, b, A);
     }
     A.L = stream_layout(b->nm_max, A.ncell);
     VX_TRY(ctx->stream_scratch.alloc(A.L.per_robot * static_cast<size_t>(b->n)));

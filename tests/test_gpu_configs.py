@@ -69,3 +69,33 @@ def test_full_horizon_bit_exact(vx, ctx, orc, n, steps):
     np.testing.assert_array_equal(got.pos, ref.pos)
     np.testing.assert_array_equal(got.vel, ref.vel)
     assert out.spring_updates == upd and out.max_speed == np.sqrt(msq)
+
+
+@pytest.mark.parametrize("dims,kernel,steps", [((5, 6, 5), "lattice", 400),    # rank-indexed one-SM kernel
+                                               ((8, 8, 9), "cluster", 300),    # rank-indexed cluster kernel
+                                               ((12, 12, 12), "stream", 60)])  # rank-indexed streaming kernel
+def test_rank_indexed_variants_bit_exact(vx, ctx, orc, dims, kernel, steps):
+    """Shapes the vertex-indexed kernels do not cover run the rank-indexed
+    variants; same bit-exactness bar (bench block + a decoded robot)."""
+    w, h, d = dims
+    rng = np.random.default_rng(w * 100 + h * 10 + d)
+    g = orc.sample_genome(32, [64, 64], int(rng.integers(0, 2 ** 62)))
+    mats, wts = vx.decode(g[0][None], g[1][None], vx.Arch.make(), w, h, d, ctx)
+    full = np.zeros(w * h * d, np.uint8)
+    for z in range(d):
+        for y in range(h):
+            for x in range(w):
+                full[x + w * (y + h * z)] = [1, 2, 3, 4][(x + 2 * y + 3 * z) % 4]  # bench.hpp:35-44 pattern
+    items = [(full, np.ones(w * h * d)), (orc.largest_component(mats[0], w, h, d), wts[0])]
+    batch = vx.build_mass_spring(np.stack([m for m, _ in items]), np.stack([x for _, x in items]), w, h, d, ctx=ctx)
+    systems = [orc.build(m, x, w, h, d) for m, x in items]
+    batch.override_phase(np.concatenate([orc.workspace(s)["sin_phase"] for s in systems]),
+                         np.concatenate([orc.workspace(s)["cos_phase"] for s in systems]))
+    out = batch.step(vx.SimConfig(), 0, steps)
+    assert ctx.last_integrator == kernel
+    got = batch.download()
+    for r, s in enumerate(systems):
+        ref, ok, called, upd, msq = orc.step(s, vx.SimConfig().as_array(), 0, steps)
+        np.testing.assert_array_equal(got.robot(r)["pos"], ref.pos, err_msg=f"{dims} robot {r}")
+        np.testing.assert_array_equal(got.robot(r)["vel"], ref.vel, err_msg=f"{dims} robot {r}")
+        assert out[r].spring_updates == upd
