@@ -316,20 +316,40 @@ def main():
     avg_int_ms = int_ms / max(1, int_n)
     achieved_tf = FLOPS_PER_UPDATE * local_upd / (avg_int_ms * 1e-3) / 1e12 if int_n else None
     peak_tf = ctx.fp64_peak_tflops()
-    default = args.workload == "config2"  # the committed ncu capture is of the config-2 kernel
-    roofline = {"bound": "fp64", "achieved": achieved_tf, "peak": peak_tf, "unit": "TFLOP/s",
-                "frac": (achieved_tf / peak_tf) if achieved_tf else None,
-                "traffic": _ncu_traffic() if default else None,
-                "kernel": args.kernel, "kernel_ms_avg": avg_int_ms,
-                "kernel_share_of_step": (int_ms / total_ms) if total_ms else None,
-                "peak_source": "measured DFMA throughput on this GPU (vx_fp64_peak; MEASURED_PEAKS.json has no "
-                               "FP64 entry), 2 flop/DFMA",
-                "algorithmic": f"{FLOPS_PER_UPDATE} FP64 flop + 1 sqrt + 1 div per spring update x "
-                               f"{local_upd} updates per launch",
-                "fp64_pipe_busy_ncu": _ncu_field("fp64_pipe_pct") if default else None,
-                "note": "parity mode forbids FMA contraction and IEEE sqrt/1/x cost ~15 FP64 instructions for 2 "
-                        "counted flop, so the flop fraction is structurally capped near 40%; fp64_pipe_busy_ncu is "
-                        "the FP64-pipe utilisation of the same kernel from the committed ncu capture"}
+    # the dominant kernel's roofline: FP64-issue bound on chip (configs 2, 3),
+    # HBM bound for the streaming integrator (config 5)
+    prof = {"config2": "integrator_traffic.json", "config3": "cluster_traffic.json",
+            "config5": "stream_traffic.json"}[args.workload]
+    meta = _ncu_json(prof)
+    launch_upd = local_upd
+    traffic = None
+    if meta.get("dram_bytes_per_launch") is not None and args.workload == "config2":
+        traffic = meta["dram_bytes_per_launch"]  # captured at the config-2 launch shape (batch load dominated)
+    elif meta.get("dram_bytes_per_update") is not None:
+        traffic = meta["dram_bytes_per_update"] * launch_upd
+    if args.workload == "config5":
+        peak_gbs, peak_src = _hbm_peak()
+        ab = meta.get("algorithmic_bytes_per_update", 60)
+        achieved_gbs = ab * launch_upd / (avg_int_ms * 1e-3) / 1e9 if int_n else None
+        roofline = {"bound": "hbm", "achieved": achieved_gbs, "peak": peak_gbs, "unit": "GB/s",
+                    "frac": (achieved_gbs / peak_gbs) if achieved_gbs else None, "traffic": traffic,
+                    "kernel": args.kernel, "kernel_ms_avg": avg_int_ms,
+                    "kernel_share_of_step": (int_ms / total_ms) if total_ms else None, "peak_source": peak_src,
+                    "algorithmic": f"{ab} B per spring update (SURVEY.md §8(d)) x {launch_upd} updates per launch",
+                    "fp64_pipe_busy_ncu": meta.get("fp64_pipe_pct")}
+    else:
+        roofline = {"bound": "fp64", "achieved": achieved_tf, "peak": peak_tf, "unit": "TFLOP/s",
+                    "frac": (achieved_tf / peak_tf) if achieved_tf else None, "traffic": traffic,
+                    "kernel": args.kernel, "kernel_ms_avg": avg_int_ms,
+                    "kernel_share_of_step": (int_ms / total_ms) if total_ms else None,
+                    "peak_source": "measured DFMA throughput on this GPU (vx_fp64_peak; MEASURED_PEAKS.json has no "
+                                   "FP64 entry), 2 flop/DFMA",
+                    "algorithmic": f"{FLOPS_PER_UPDATE} FP64 flop + 1 sqrt + 1 div per spring update x "
+                                   f"{local_upd} updates per launch",
+                    "fp64_pipe_busy_ncu": meta.get("fp64_pipe_pct"),
+                    "note": "parity mode forbids FMA contraction and IEEE sqrt/1/x cost ~15 FP64 instructions for 2 "
+                            "counted flop, so the flop fraction is structurally capped near 40%; fp64_pipe_busy_ncu "
+                            "is the FP64-pipe utilisation of the same kernel from the committed ncu capture"}
 
     cpu = None
     if world == 1 and not args.no_cpu_baseline and not args.profile:
@@ -368,20 +388,22 @@ def main():
         dist.destroy_process_group()
 
 
-def _ncu_field(key):
-    """A field of the committed ncu capture of the integrator (profiles/integrator_traffic.json)."""
-    path = os.path.join(ROOT, "profiles", "integrator_traffic.json")
-    if os.path.exists(path):
-        try:
-            return json.load(open(path)).get(key)
-        except Exception:
-            return None
-    return None
+def _ncu_json(name):
+    """Figures from a committed ncu capture of the workload's integrator (profiles/*.json)."""
+    path = os.path.join(ROOT, "profiles", name)
+    try:
+        return json.load(open(path))
+    except Exception:
+        return {}
 
 
-def _ncu_traffic():
-    """dram bytes per integrator launch from the committed ncu capture, if any."""
-    return _ncu_field("dram_bytes_per_launch")
+def _hbm_peak():
+    """Measured HBM copy bandwidth (MEASURED_PEAKS.json, driver-written), else the profiling guide's figure."""
+    try:
+        return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]), \
+            "MEASURED_PEAKS.json hbm_gbs (measured copy bandwidth)"
+    except Exception:
+        return 6556.5, "B200_PROFILING.md fallback"
 
 
 if __name__ == "__main__":
