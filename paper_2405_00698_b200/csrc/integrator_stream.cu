@@ -704,6 +704,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_sym_kernel(SymArgs A
                     if (d < 0) break;
                     const int off = key_off<VW>(d);
                     const double* Xi = Xk - off;
+                    VX_DCHECK(PAD + key - off >= 0 && VOX[d * PCOL + key] < NT);
                     force(Xi[0], Xi[XS], Xi[2 * XS], Xi[3 * XS], Xi[4 * XS], Xi[5 * XS], Xk, K[d * PCOL + key],
                           R0[d * PCOL + key], VOX[d * PCOL + key], (bmask >> d) & 1u, of[q]);
                 }
@@ -728,6 +729,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_sym_kernel(SymArgs A
                     const int d = c0 + q;
                     if (d > 12) break;
                     const int off = key_off<VW>(d);
+                    VX_DCHECK(key + off < PCOL && PAD + key + off < XS && VOX[d * PCOL + key + off] < NT);
                     force(x0, x1, x2, v0, v1, v2, Xk + off, K[d * PCOL + key + off], R0[d * PCOL + key + off],
                           VOX[d * PCOL + key + off], (fmask >> d) & 1u, of[q]);
                 }
