@@ -140,11 +140,11 @@ def resume_run(checkpoint_path: str, rc: RunConfig, ctx: Optional[Context] = Non
 
 
 def main(argv=None) -> int:
-    """``python -m paper_2405_00698_b200.runner run.json [--resume checkpoint.json]``:
+    """``python -m paper_2405_00698_b200 run.json [--resume checkpoint.json]``:
     the reference CLI's run / resume over this build (voxevo_main.cpp)."""
     import argparse
     from .serialize import load_run_config
-    ap = argparse.ArgumentParser(prog="python -m paper_2405_00698_b200.runner")
+    ap = argparse.ArgumentParser(prog="python -m paper_2405_00698_b200")
     ap.add_argument("config")
     ap.add_argument("--resume", default=None)
     a = ap.parse_args(argv)
