@@ -53,17 +53,24 @@ class CheckpointError(RuntimeError):
 
 
 # ------------------------------------------------------ canonical JSON dump
-def format_doubles(values) -> list:
-    """nlohmann::json number text of each double (vx_format_doubles)."""
+def format_doubles_text(values, sep: str = ",") -> str:
+    """nlohmann::json number text of each double, joined by `sep` (vx_format_doubles)."""
     v = np.ascontiguousarray(values, dtype=np.float64).ravel()
     if v.size == 0:
-        return []
+        return ""
     cap = 26 * v.size + 1
     buf = C.create_string_buffer(cap)
     n = _lib().vx_format_doubles(v.ctypes.data, v.size, b",", buf, cap)
     if n < 0 or n >= cap:
         raise RuntimeError("vx_format_doubles failed")
-    return buf.raw[:n].decode().split(",")
+    text = buf.raw[:n].decode()
+    return text if sep == "," else text.replace(",", sep)
+
+
+def format_doubles(values) -> list:
+    """nlohmann::json number text of each double (vx_format_doubles)."""
+    text = format_doubles_text(values)
+    return text.split(",") if text else []
 
 
 def _fmt_double(x: float) -> str:
@@ -71,17 +78,12 @@ def _fmt_double(x: float) -> str:
 
 
 def _is_float_list(seq) -> bool:
-    return len(seq) > 0 and all(isinstance(x, (float, np.floating)) for x in seq)
-
-
-class _Raw(str):
-    """Pre-formatted number text."""
+    return len(seq) > 0 and isinstance(seq[0], (float, np.floating)) and \
+        all(isinstance(x, (float, np.floating)) and not isinstance(x, bool) for x in seq)
 
 
 def _dump(v: Any, out: list, indent: Optional[int], level: int):
-    if isinstance(v, _Raw):
-        out.append(str(v))
-    elif v is None:
+    if v is None:
         out.append("null")
     elif v is True:
         out.append("true")
@@ -116,12 +118,18 @@ def _dump(v: Any, out: list, indent: Optional[int], level: int):
                 _dump(v[key], out, indent, level + 1)
             out.append("\n" + pad + "}")
     elif isinstance(v, (list, tuple, np.ndarray)):
-        seq = list(v)
-        if not seq:
+        seq = v if isinstance(v, np.ndarray) else list(v)
+        if len(seq) == 0:
             out.append("[]")
             return
-        if _is_float_list(seq):  # genome tensors: one library call per tensor
-            seq = [_Raw(t) for t in format_doubles(seq)]
+        if (isinstance(seq, np.ndarray) and seq.dtype == np.float64) or _is_float_list(seq):
+            # genome tensors: one library call per tensor, numbers never contain ','
+            if indent is None:
+                out.append("[" + format_doubles_text(seq) + "]")
+            else:
+                pad, inner = " " * (indent * level), " " * (indent * (level + 1))
+                out.append("[\n" + inner + format_doubles_text(seq, ",\n" + inner) + "\n" + pad + "]")
+            return
         if indent is None:
             out.append("[")
             for i, x in enumerate(seq):
@@ -412,8 +420,10 @@ def genome_to_json(params: np.ndarray, bmat: np.ndarray, arch: Arch) -> dict:
         o += fan_in * fan_out
         b = params[o:o + fan_out]
         o += fan_out
-        layers.append({"in": fan_in, "out": fan_out, "w": [float(x) for x in w], "b": [float(x) for x in b]})
-    return {"encoding": {"m": int(arch.m), "d": 3, "sigma": _f(arch.sigma)}, "b_matrix": [float(x) for x in bmat],
+        layers.append({"in": fan_in, "out": fan_out, "w": np.asarray(w, np.float64).tolist(),
+                       "b": np.asarray(b, np.float64).tolist()})
+    return {"encoding": {"m": int(arch.m), "d": 3, "sigma": _f(arch.sigma)},
+            "b_matrix": np.asarray(bmat, np.float64).tolist(),
             "hidden": layers[:-2], "head_material": layers[-2], "head_weight": layers[-1]}
 
 
