@@ -242,7 +242,7 @@ def main():
     init_params = torch.from_numpy(pop0["params"]).cuda()
     init_bmat = torch.from_numpy(pop0["bmat"]).cuda()
     del pop0
-    xbuf = torch.zeros(2 * P, dtype=torch.float64, device="cuda")
+    xbuf = torch.zeros(st.exchange_buffer()[1], dtype=torch.float64, device="cuda")  # fitness|updates|histogram
     st.set_exchange_buffer(xbuf.data_ptr())
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
     host_params = torch.empty((P, np_), dtype=torch.float64, pin_memory=True)

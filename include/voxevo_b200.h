@@ -242,17 +242,21 @@ vx_status vx_evo_free(vx_evo* e);
 /* evolve_generation (evolution.hpp:217-293), advisor off (the shim calls the
  * advisor between generations and applies vx_evo_set_params). */
 vx_status vx_evo_generation(vx_evo* e, vx_report* rep);
-/* Sharded form: begin() decodes children (replicated) and
- * evaluates the children assigned to `rank` of `world`; the caller then
- * all-reduces (sum) the P-long fitness/flag exchange buffer (device,
- * vx_evo_exchange_buffer) across ranks; finish() sorts, reports and breeds
- * (replicated, identical on every rank). */
+/* Sharded form: begin() decodes and evaluates the children
+ * assigned to `rank` of `world` (strided over the todo list; no grid ever
+ * moves: every rank derives the same owner map) and writes this rank's part
+ * of the exchange buffer; the caller then all-reduces (sum) the buffer
+ * (device, vx_evo_exchange_buffer) across ranks; finish() sorts, reports and
+ * breeds (replicated, identical on every rank). */
 vx_status vx_evo_begin(vx_evo* e, int32_t rank, int32_t world);
-/* d_buf: P doubles (fitness of locally evaluated children, 0 elsewhere)
- * followed by P doubles of per-robot spring updates; n_doubles = 2P. */
+/* d_buf: P doubles (fitness of locally evaluated children, 0 elsewhere),
+ * P doubles of per-robot spring updates, then cells x 5 material counts over
+ * the individuals whose grid this rank owns (the population diversity is a
+ * function of the summed counts); n_doubles = 2P + 5 cells. */
 vx_status vx_evo_exchange_buffer(vx_evo* e, double** d_buf, int64_t* n_doubles);
-/* Use a caller-owned device buffer of 2P doubles (e.g. a torch tensor that
- * torch.distributed all-reduces over NCCL) as the exchange buffer. */
+/* Use a caller-owned device buffer of n_doubles (vx_evo_exchange_buffer; e.g.
+ * a torch tensor that torch.distributed all-reduces over NCCL) as the
+ * exchange buffer. */
 vx_status vx_evo_set_exchange_buffer(vx_evo* e, double* d_buf);
 /* Generation-0 reset from DEVICE arrays (P x np params, P x 3m B): fitness,
  * evaluated flags and cached grids are cleared (init_evolution state). */

@@ -715,7 +715,7 @@ class EvolutionState:
         return int(p.value or 0), int(n.value)
 
     def set_exchange_buffer(self, d_ptr: int):
-        """Use a caller-owned device buffer of 2P doubles (e.g. a torch tensor
+        """Use a caller-owned device buffer of exchange_buffer()[1] doubles (e.g. a torch tensor
         that torch.distributed all-reduces) as the exchange buffer."""
         _check(_lib().vx_evo_set_exchange_buffer(self.h, d_ptr))
 

@@ -68,6 +68,9 @@ struct vx_evo {
     DevBuf<double> prm[2], bm[2], fit[2], gw[2];
     DevBuf<uint8_t> ev[2], grid[2];
     std::vector<uint8_t> h_eval, h_has_grid;
+    // rank that holds an individual's decoded grid (sharded decode; -1: none)
+    std::vector<int32_t> h_owner;
+    DevBuf<int32_t> d_own;
     // generation scratch
     DevBuf<int32_t> d_todo, d_dec, perm, iota;
     DevBuf<double> xbuf, sorted, keys_tmp, stats, div;
@@ -104,6 +107,11 @@ struct vx_evo {
 };
 
 namespace {
+
+// exchange buffer: [fitness P | spring updates P | material histogram cells x NMAT]
+size_t xbuf_doubles(const vx_evo* e) {
+    return 2 * static_cast<size_t>(e->P) + static_cast<size_t>(e->cells) * VX_NMAT;
+}
 
 // Rng::uniform01 / normal / index (rng.hpp:23-39) on the GA stream.
 inline double u01(std::mt19937_64& r) { return static_cast<double>(r() >> 11) * 0x1.0p-53; }
@@ -187,7 +195,7 @@ vx_status alloc_evo(vx_evo* e) {
     VX_TRY(e->d_dec.alloc(P));
     VX_TRY(e->perm.alloc(P));
     VX_TRY(e->iota.alloc(P));
-    VX_TRY(e->xbuf.alloc(2 * P));
+    VX_TRY(e->xbuf.alloc(2 * static_cast<size_t>(P) + static_cast<size_t>(e->cells) * VX_NMAT));
     VX_TRY(e->sorted.alloc(P));
     VX_TRY(e->keys_tmp.alloc(P));
     VX_TRY(e->stats.alloc(4));
@@ -198,6 +206,8 @@ vx_status alloc_evo(vx_evo* e) {
     e->mask_words = (e->np + 31) / 32;
     e->h_eval.assign(P, 0);
     e->h_has_grid.assign(P, 0);
+    e->h_owner.assign(P, -1);
+    VX_TRY(e->d_own.alloc(P));
     return VX_OK;
 }
 
@@ -268,30 +278,61 @@ vx_status vx_evo_begin(vx_evo* e, int32_t rank, int32_t world) {
     e->table.k_bone *= e->params.material_multipliers[2];
     // breeding plan parse overlaps everything below
     start_plan(e);
-    // decode individuals without a cached grid (evolution.hpp:230-236)
-    std::vector<int32_t> dec;
+    // decode individuals without a cached grid (evolution.hpp:230-236),
+    // sharded: an individual to evaluate is decoded by the rank that evaluates
+    // it (strided over the todo list); grids needed only for the diversity
+    // (elites restored without one) are striped over the remaining list.
+    // Every rank derives the same owner map, so no grid ever moves.
+    std::vector<int32_t> dec_rest;
     e->todo.clear();
     for (int a = 0; a < e->P; ++a) {
-        if (!e->h_has_grid[a]) dec.push_back(a);
         if (!e->h_eval[a]) e->todo.push_back(a);
+        else if (!e->h_has_grid[a]) dec_rest.push_back(a);
+    }
+    std::vector<int32_t> dec, mine;
+    for (size_t q = 0; q < e->todo.size(); ++q) {
+        const int a = e->todo[q];
+        const int owner = static_cast<int>(q % static_cast<size_t>(world));
+        if (owner == rank) mine.push_back(a);  // this rank's shard of the evaluations
+        if (!e->h_has_grid[a]) {
+            e->h_owner[a] = owner;
+            e->h_has_grid[a] = 1;
+            if (owner == rank) dec.push_back(a);
+        }
+    }
+    for (size_t q = 0; q < dec_rest.size(); ++q) {
+        const int a = dec_rest[q];
+        const int owner = static_cast<int>(q % static_cast<size_t>(world));
+        e->h_owner[a] = owner;
+        e->h_has_grid[a] = 1;
+        if (owner == rank) dec.push_back(a);
     }
     if (!dec.empty()) {
         VX_CUDA(cudaMemcpyAsync(e->d_dec.p, dec.data(), dec.size() * sizeof(int32_t), cudaMemcpyHostToDevice,
                                 ctx->stream));
         VX_TRY(decode_dev(ctx, &e->cfg.arch, e->P, e->prm[c].p, e->bm[c].p, e->cfg.grid_w, e->cfg.grid_h,
                           e->cfg.grid_d, e->grid[c].p, e->gw[c].p, nullptr, e->d_dec.p, static_cast<int>(dec.size())));
-        for (int a : dec) e->h_has_grid[a] = 1;
     }
-    // this rank's shard of the evaluations (strided over the todo list)
-    std::vector<int32_t> mine;
-    for (size_t q = rank; q < e->todo.size(); q += world) mine.push_back(e->todo[q]);
-    VX_CUDA(cudaMemsetAsync(e->xb(), 0, 2 * e->P * sizeof(double), ctx->stream));
+    VX_CUDA(cudaMemsetAsync(e->xb(), 0, xbuf_doubles(e) * sizeof(double), ctx->stream));
     if (!mine.empty()) {
         VX_CUDA(cudaMemcpyAsync(e->d_todo.p, mine.data(), mine.size() * sizeof(int32_t), cudaMemcpyHostToDevice,
                                 ctx->stream));
         VX_TRY(evaluate_pipeline(ctx, e->P, e->cfg.grid_w, e->cfg.grid_h, e->cfg.grid_d, e->grid[c].p, e->gw[c].p,
                                  &e->table, &e->cfg.plane, &e->cfg.sim, e->d_todo.p, static_cast<int>(mine.size()),
                                  e->xb(), e->xb() + e->P, nullptr));
+    }
+    // this rank's part of the population material histogram (the diversity is
+    // a function of it, population_diversity evolution.hpp:89-105): summed
+    // over ranks with the fitness vector in the exchange buffer
+    {
+        std::vector<int32_t> own;
+        for (int a = 0; a < e->P; ++a)
+            if (e->h_owner[a] == rank) own.push_back(a);
+        if (!own.empty())
+            VX_CUDA(cudaMemcpyAsync(e->d_own.p, own.data(), own.size() * sizeof(int32_t), cudaMemcpyHostToDevice,
+                                    ctx->stream));
+        VX_TRY(histogram_sel_dev(ctx, static_cast<int>(own.size()), e->d_own.p, e->cells, e->grid[c].p,
+                                 e->xb() + 2 * e->P));
     }
     // the todo list (all ranks) goes to the device for the merge
     if (!e->todo.empty())
@@ -304,7 +345,7 @@ vx_status vx_evo_begin(vx_evo* e, int32_t rank, int32_t world) {
 vx_status vx_evo_exchange_buffer(vx_evo* e, double** d_buf, int64_t* n_doubles) {
     if (!e || !d_buf) return VX_EINVAL;
     *d_buf = e->xb();
-    if (n_doubles) *n_doubles = 2LL * e->P;
+    if (n_doubles) *n_doubles = static_cast<int64_t>(xbuf_doubles(e));
     return VX_OK;
 }
 
@@ -327,6 +368,7 @@ vx_status vx_evo_load_population_dev(vx_evo* e, const double* d_params, const do
     VX_CUDA(cudaMemsetAsync(e->ev[c].p, 0, P, s));
     std::fill(e->h_eval.begin(), e->h_eval.end(), 0);
     std::fill(e->h_has_grid.begin(), e->h_has_grid.end(), 0);
+    std::fill(e->h_owner.begin(), e->h_owner.end(), -1);
     return VX_OK;
 }
 
@@ -337,7 +379,7 @@ vx_status vx_evo_finish(vx_evo* e, vx_report* rep) {
     const int c = e->cur, nx = 1 - c, P = e->P;
     VX_TRY(merge_dev(ctx, static_cast<int>(e->todo.size()), e->d_todo.p, e->xb(), e->fit[c].p, e->ev[c].p));
     VX_TRY(sort_stats_dev(ctx, P, e->fit[c].p, e->perm.p, e->sorted.p, e->iota.p, e->keys_tmp.p, e->stats.p));
-    VX_TRY(histogram_dev(ctx, P, e->cells, e->grid[c].p, e->hist.p, false));
+    VX_TRY(hist_from_doubles_dev(ctx, e->cells, e->xb() + 2 * P, e->hist.p));  // summed over ranks
     VX_TRY(diversity_from_hist_dev(ctx, P, e->cells, e->hist.p, e->div.p));
     double st[3], div = 0.0;
     std::vector<double> upd(e->todo.empty() ? 0 : P);
@@ -408,7 +450,16 @@ vx_status vx_evo_finish(vx_evo* e, vx_report* rep) {
     A.dst_grid = e->grid[nx].p;
     A.dst_gridw = e->gw[nx].p;
     VX_TRY(breed_dev(ctx, A, P, e->d_mut.p, static_cast<int64_t>(e->h_mut.size())));
-    // host mirrors: elites are evaluated and keep their grids; children are fresh
+    // host mirrors: elites are evaluated and keep their grids (and owners);
+    // children are fresh
+    std::vector<int32_t> elite_src(static_cast<size_t>(n_elite));
+    if (n_elite > 0)
+        VX_CUDA(cudaMemcpyAsync(elite_src.data(), e->perm.p, n_elite * sizeof(int32_t), cudaMemcpyDeviceToHost,
+                                ctx->stream));
+    VX_CUDA(cudaStreamSynchronize(ctx->stream));
+    std::vector<int32_t> owner_next(static_cast<size_t>(P), -1);
+    for (int a = 0; a < n_elite; ++a) owner_next[a] = e->h_owner[elite_src[a]];
+    e->h_owner.swap(owner_next);
     for (int a = 0; a < P; ++a) {
         e->h_eval[a] = a < n_elite ? 1 : 0;
         e->h_has_grid[a] = a < n_elite ? 1 : 0;
@@ -475,6 +526,7 @@ vx_status vx_evo_set_population(vx_evo* e, const double* params, const double* b
     for (size_t a = 0; a < P; ++a) {
         e->h_eval[a] = ev[a] ? 1 : 0;
         e->h_has_grid[a] = grids ? 1 : 0;
+        e->h_owner[a] = grids ? 0 : -1;  // host-provided grids: rank 0's copy counts
     }
     return VX_OK;
 }

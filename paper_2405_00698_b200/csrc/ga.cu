@@ -38,6 +38,25 @@ __global__ void hist_kernel(int P, int cells, const uint8_t* __restrict__ mat, i
     for (int k = 0; k < VX_NMAT; ++k) hist[c * VX_NMAT + k] = (accumulate ? hist[c * VX_NMAT + k] : 0) + n[k];
 }
 
+// counts over a list of individuals (this rank's share), as doubles for the
+// exchange-buffer all-reduce (exact: counts < 2^53)
+__global__ void hist_sel_kernel(int n, const int32_t* __restrict__ sel, int cells, const uint8_t* __restrict__ mat,
+                                double* __restrict__ out) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= cells) return;
+    int64_t cnt[VX_NMAT] = {0, 0, 0, 0, 0};
+    for (int q = 0; q < n; ++q) {
+        const int m = mat[static_cast<size_t>(sel[q]) * cells + c];
+        if (m < VX_NMAT) cnt[m] += 1;
+    }
+    for (int k = 0; k < VX_NMAT; ++k) out[c * VX_NMAT + k] = static_cast<double>(cnt[k]);
+}
+
+__global__ void hist_from_doubles_kernel(int n, const double* __restrict__ in, int64_t* __restrict__ out) {
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q < n) out[q] = static_cast<int64_t>(in[q]);
+}
+
 __global__ void diversity_kernel(int P, int cells, const int64_t* __restrict__ hist, double* out) {
     __shared__ unsigned long long s_tot;
     if (threadIdx.x == 0) s_tot = 0ull;
@@ -68,6 +87,24 @@ __global__ void diversity_kernel(int P, int cells, const int64_t* __restrict__ h
 vx_status histogram_dev(vx_ctx* ctx, int P, int cells, const uint8_t* d_mat, int64_t* d_hist, bool accumulate) {
     if (cells <= 0) return VX_OK;
     hist_kernel<<<ceil_div(cells, kThreads), kThreads, 0, ctx->stream>>>(P, cells, d_mat, d_hist, accumulate ? 1 : 0);
+    ctx->launches++;
+    VX_CUDA(cudaGetLastError());
+    return VX_OK;
+}
+
+vx_status histogram_sel_dev(vx_ctx* ctx, int n_sel, const int32_t* d_sel, int cells, const uint8_t* d_mat,
+                            double* d_out) {
+    if (cells <= 0) return VX_OK;
+    hist_sel_kernel<<<ceil_div(cells, kThreads), kThreads, 0, ctx->stream>>>(n_sel, d_sel, cells, d_mat, d_out);
+    ctx->launches++;
+    VX_CUDA(cudaGetLastError());
+    return VX_OK;
+}
+
+vx_status hist_from_doubles_dev(vx_ctx* ctx, int cells, const double* d_in, int64_t* d_out) {
+    const int n = cells * VX_NMAT;
+    if (n <= 0) return VX_OK;
+    hist_from_doubles_kernel<<<ceil_div(n, kThreads), kThreads, 0, ctx->stream>>>(n, d_in, d_out);
     ctx->launches++;
     VX_CUDA(cudaGetLastError());
     return VX_OK;

@@ -7,7 +7,7 @@
   --config4: P=65536, 10^3, sharded over W GPUs: one GPU's share of a
              generation (vx_evo_begin(rank 0, W): decode + evaluate of every
              W-th child) timed for W in --worlds; the all-reduce of the
-             2P-double exchange buffer and finish() are not part of the shard
+             exchange buffer and finish() are not part of the shard
              time (finish is timed separately on the full-population state).
 """
 import argparse
@@ -47,7 +47,7 @@ def config4(worlds, steps):
     P = 65536
     cfg = vx.EvolutionConfig(population=P, grid=(10, 10, 10), seed=42, sim=vx.SimConfig(duration=steps * 1e-5))
     st = vx.init_evolution(cfg, ctx)
-    xbuf = torch.zeros(2 * P, dtype=torch.float64, device="cuda")  # [fitness P | spring updates P]
+    xbuf = torch.zeros(st.exchange_buffer()[1], dtype=torch.float64, device="cuda")  # [fitness|updates|histogram]
     st.set_exchange_buffer(xbuf.data_ptr())
     for w in worlds:
         xbuf.zero_()

@@ -131,3 +131,37 @@ def test_population_beyond_grid_y_limit(vx, ctx):
     r1 = st.evolve_generation()
     assert r0.evaluations == 70000 and r1.evaluations == 70000 - vx.elite_count(0.3, 70000)
     assert r1.best >= r0.best
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_generation_matches_single_process(vx, ctx, world):
+    """vx_evo_begin(rank, world) on `world` replicas (one GPU, ranks run one
+    after another), a summed exchange buffer standing in for the NCCL
+    all-reduce, then finish() everywhere: reports, populations and RNG streams
+    equal the single-process run bit for bit — decode and evaluation sharded,
+    diversity from the summed material histogram."""
+    import torch
+    cfg = desk(vx, 77, P=12, gens=4)
+    single = vx.init_evolution(cfg, ctx)
+    ranks = [vx.init_evolution(cfg, ctx) for _ in range(world)]
+    n = ranks[0].exchange_buffer()[1]
+    assert n == 2 * 12 + 5 * 27
+    bufs = [torch.zeros(n, dtype=torch.float64, device="cuda") for _ in range(world)]
+    for st, b in zip(ranks, bufs):
+        st.set_exchange_buffer(b.data_ptr())
+    key = lambda r: (r.generation, r.best, r.mean, r.stddev, r.diversity, r.evaluations, int(r.spring_updates))
+    for _ in range(4):
+        ref = single.evolve_generation()
+        for r, st in enumerate(ranks):
+            st.begin(r, world)
+        ctx.synchronize()
+        torch.cuda.synchronize()
+        total = torch.stack(bufs).sum(0)
+        for b in bufs:
+            b.copy_(total)
+        torch.cuda.synchronize()
+        for st in ranks:
+            assert key(st.finish()) == key(ref)
+    for st in ranks:
+        assert st.rng_state() == single.rng_state()
+        np.testing.assert_array_equal(st.population()["params"], single.population()["params"])
