@@ -58,6 +58,16 @@ vx_status evaluate_pipeline(vx_ctx* ctx, int P, int w, int h, int d, const uint8
 
 }  // namespace vx
 
+namespace {
+// MutStore chunk memory: pinned, so the per-generation mutation upload is an
+// asynchronous DMA straight from the chunks the plan thread wrote
+void* pinned_alloc(size_t n) {
+    void* p = nullptr;
+    return cudaMallocHost(&p, n) == cudaSuccess ? p : nullptr;
+}
+void pinned_free(void* p) { cudaFreeHost(p); }
+}  // namespace
+
 struct vx_evo {
     vx_ctx* ctx = nullptr;
     vx_evo_config cfg{};
@@ -82,11 +92,13 @@ struct vx_evo {
     DevBuf<MutEntry> d_mut;
     std::vector<ChildPlan> h_plan;
     std::vector<uint32_t> h_masks;
-    std::vector<MutEntry> h_mut;
+    MutStore h_mut{pinned_alloc, pinned_free};
+    cudaEvent_t mut_uploaded = nullptr;  // the previous plan's async upload has read h_mut
     int64_t mask_words = 0;
     int plan_elite = 0;
     std::thread plan_thread;
     bool plan_running = false;
+    bool plan_failed = false;  // host allocation failed inside the plan thread
     std::mt19937_64 rng;
     int generation = 0;
     double best_fitness = 0.0;
@@ -103,6 +115,7 @@ struct vx_evo {
 
     ~vx_evo() {
         if (plan_thread.joinable()) plan_thread.join();
+        if (mut_uploaded) cudaEventDestroy(mut_uploaded);
     }
 };
 
@@ -113,56 +126,17 @@ size_t xbuf_doubles(const vx_evo* e) {
     return 2 * static_cast<size_t>(e->P) + static_cast<size_t>(e->cells) * VX_NMAT;
 }
 
-// Rng::uniform01 / normal / index (rng.hpp:23-39) on the GA stream.
-inline double u01(std::mt19937_64& r) { return static_cast<double>(r() >> 11) * 0x1.0p-53; }
-inline double normal(std::mt19937_64& r) {
-    const double u1 = (static_cast<double>(r() >> 11) + 0.5) * 0x1.0p-53;
-    const double u2 = static_cast<double>(r() >> 11) * 0x1.0p-53;
-    return std::sqrt(-2.0 * std::log(u1)) * std::cos(2.0 * M_PI * u2);
-}
-inline uint64_t index(std::mt19937_64& r, uint64_t n) {
-    const uint64_t threshold = (0 - n) % n;
-    for (;;) {
-        const uint64_t x = r();
-        if (x >= threshold) return x % n;
-    }
-}
-// tournament_select (evolution.hpp:169-173) -> sorted rank
-inline int32_t tournament(std::mt19937_64& r, int P, int size) {
-    uint64_t winner = index(r, static_cast<uint64_t>(P));
-    for (int k = 1; k < size; ++k) winner = std::min<uint64_t>(winner, index(r, static_cast<uint64_t>(P)));
-    return static_cast<int32_t>(winner);
-}
-
 // Breeding loop (evolution.hpp:267-289) in rank space: consumes the GA
-// stream draw-for-draw like the reference.
+// stream draw-for-draw like the reference (ga_plan.cpp).
 void parse_plan(vx_evo* e) {
-    const int P = e->P;
-    const int n_elite = vx_elite_count(e->params.elite_fraction, P);
+    const int n_elite = vx_elite_count(e->params.elite_fraction, e->P);
     e->plan_elite = n_elite;
-    const int n_child = P - n_elite;
-    e->h_plan.resize(std::max(1, n_child));
-    e->h_masks.clear();
-    e->h_mut.clear();
-    int slots = 0;
-    const double cx_rate = e->params.crossover_rate, rate = e->params.mutation_rate, scale = e->params.mutation_scale;
-    for (int c = n_elite; c < P; ++c) {
-        ChildPlan& p = e->h_plan[c - n_elite];
-        p.pa = tournament(e->rng, P, e->cfg.tournament_size);
-        p.pb = -1;
-        p.mask_slot = -1;
-        p.pad = 0;
-        if (u01(e->rng) < cx_rate) {
-            p.pb = tournament(e->rng, P, e->cfg.tournament_size);
-            p.mask_slot = slots++;
-            const size_t base = e->h_masks.size();
-            e->h_masks.resize(base + e->mask_words, 0u);
-            uint32_t* m = e->h_masks.data() + base;
-            for (int64_t i = 0; i < e->np; ++i)  // crossover (evolution.hpp:143-155)
-                if (u01(e->rng) < 0.5) m[i >> 5] |= 1u << (i & 31);
-        }
-        for (int64_t i = 0; i < e->np; ++i)  // mutate (evolution.hpp:160-165)
-            if (u01(e->rng) < rate) e->h_mut.push_back(MutEntry{c, static_cast<int32_t>(i), normal(e->rng) * scale});
+    const PlanParams a{e->P, n_elite, e->cfg.tournament_size, e->np, e->mask_words, e->params.crossover_rate,
+                       e->params.mutation_rate, e->params.mutation_scale};
+    try {
+        plan_scan(e->rng, a, e->h_plan, e->h_masks, e->h_mut);
+    } catch (const std::bad_alloc&) {
+        e->plan_failed = true;
     }
 }
 
@@ -212,7 +186,10 @@ vx_status alloc_evo(vx_evo* e) {
 }
 
 void start_plan(vx_evo* e) {
+    // the previous generation's upload reads h_mut asynchronously
+    if (e->mut_uploaded) cudaEventSynchronize(e->mut_uploaded);
     e->plan_running = true;
+    e->plan_failed = false;
     e->plan_thread = std::thread([e] { parse_plan(e); });
 }
 
@@ -414,6 +391,7 @@ vx_status vx_evo_finish(vx_evo* e, vx_report* rep) {
     r.spring_updates = total;
     // breed (evolution.hpp:267-289)
     join_plan(e);
+    if (e->plan_failed) return (set_error("breeding plan: host allocation failed"), VX_EOOM);
     const int n_elite = e->plan_elite;
     const int n_child = P - n_elite;
     VX_TRY(e->d_plan.alloc(std::max(1, n_child)));
@@ -425,9 +403,11 @@ vx_status vx_evo_finish(vx_evo* e, vx_report* rep) {
     if (!e->h_masks.empty())
         VX_CUDA(cudaMemcpyAsync(e->d_masks.p, e->h_masks.data(), e->h_masks.size() * sizeof(uint32_t),
                                 cudaMemcpyHostToDevice, ctx->stream));
-    if (!e->h_mut.empty())
-        VX_CUDA(cudaMemcpyAsync(e->d_mut.p, e->h_mut.data(), e->h_mut.size() * sizeof(MutEntry),
-                                cudaMemcpyHostToDevice, ctx->stream));
+    for (size_t j = 0; j < e->h_mut.chunks(); ++j)  // pinned chunks: true async copies
+        VX_CUDA(cudaMemcpyAsync(e->d_mut.p + j * MutStore::kChunk, e->h_mut.chunk(j),
+                                e->h_mut.chunk_size(j) * sizeof(MutEntry), cudaMemcpyHostToDevice, ctx->stream));
+    if (!e->mut_uploaded) VX_CUDA(cudaEventCreateWithFlags(&e->mut_uploaded, cudaEventDisableTiming));
+    VX_CUDA(cudaEventRecord(e->mut_uploaded, ctx->stream));
     BreedArgs A{};
     A.n_elite = n_elite;
     A.np = e->np;

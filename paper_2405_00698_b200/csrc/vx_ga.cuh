@@ -4,24 +4,10 @@
 
 #include <cstdint>
 
+#include "ga_plan.hpp"
 #include "vx_internal.cuh"
 
 namespace vx {
-
-// One child's breeding decisions in SORTED-rank space (evolution.hpp:274-282).
-struct ChildPlan {
-    int32_t pa;         // tournament winner rank (tournament_select, :169-173)
-    int32_t pb;         // second parent rank or -1 (no crossover)
-    int32_t mask_slot;  // crossover mask row (valid when pb >= 0)
-    int32_t pad;
-};
-
-// A mutated parameter: child slot, flat parameter index, delta = normal*scale.
-struct MutEntry {
-    int32_t child;
-    int32_t index;
-    double delta;
-};
 
 struct BreedArgs {
     int n_elite;
