@@ -206,6 +206,17 @@ vx_status vx_batch_step(vx_ctx* ctx, vx_batch* b, const vx_sim* sim, int64_t k0,
  * steps from t = 0 on a private copy of the state (the batch is not
  * modified, like the reference's by-value argument). */
 vx_status vx_batch_simulate(vx_ctx* ctx, vx_batch* b, const vx_sim* sim, vx_summary* summaries);
+/* simulate() with its trajectory dump (physics.hpp:280-311): for each robot
+ * the (t, com x, com y, com z) rows the reference pushes — one every `stride`
+ * steps before that step (stride <= 0: none) while the robot has not
+ * diverged, then the final row at t = n_steps*dt — written to samples
+ * (host, n x cap x 4 doubles; rows beyond cap are counted, not written) with
+ * the per-robot row count in counts (host, n).  cap for no truncation:
+ * ceil(n_steps / stride) + 1.  A robot without masses gets no rows and a
+ * zero summary.  The batch is not modified.  Bit-identical to the
+ * reference's simulate(sys, cfg, &dump, stride) on identical systems. */
+vx_status vx_batch_simulate_dump(vx_ctx* ctx, vx_batch* b, const vx_sim* sim, int32_t stride, int64_t cap,
+                                 double* samples, int64_t* counts, vx_summary* summaries);
 /* Device-pointer variant: summaries written to d_summaries (n entries). */
 vx_status vx_batch_simulate_dev(vx_ctx* ctx, vx_batch* b, const vx_sim* sim, vx_summary* d_summaries);
 

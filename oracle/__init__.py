@@ -16,6 +16,7 @@ may import this package.  The product (``paper_2405_00698_b200``) never does.
 """
 from __future__ import annotations
 
+import math
 import ctypes as C
 import os
 import subprocess
@@ -291,20 +292,33 @@ class _Lib:
             self._sys_free(h)
         return out, int(ok), int(called.value), int(upd.value), float(msq.value)
 
-    def simulate(self, s: System, sim=None) -> dict:
-        """simulate (physics.hpp:287-311)."""
+    def simulate(self, s: System, sim=None, stride=None) -> dict:
+        """simulate (physics.hpp:287-311); with ``stride`` (reference library
+        only) also the TrajectorySample dump as an (rows, 4) array."""
         sim = DEFAULT_SIM if sim is None else np.ascontiguousarray(sim, np.float64)
         h = self._make(s)
         summ = np.zeros(9)
+        dump = None
         try:
-            if self.pre == "ref_":
+            if stride is not None:
+                if self.pre != "ref_":
+                    raise RuntimeError("the trajectory dump needs the reference library (oracle/_ref)")
+                n_steps = int(math.floor(sim[2] / sim[1] + 0.5))  # llround
+                cap = (-(-n_steps // stride) if stride > 0 else 0) + 1
+                dump = np.zeros((cap, 4))
+                rows = self._simulate(h, sim.ctypes.data, summ.ctypes.data, dump.ctypes.data, cap, int(stride))
+                dump = dump[:min(int(rows), cap)].copy()
+            elif self.pre == "ref_":
                 self._simulate(h, sim.ctypes.data, summ.ctypes.data, None, 0, 0)
             else:
                 self._simulate(h, sim.ctypes.data, summ.ctypes.data)
         finally:
             self._sys_free(h)
-        return dict(com_start=summ[0:3].copy(), com_end=summ[3:6].copy(), horizontal_displacement=float(summ[6]),
-                    max_speed=float(summ[7]), diverged=bool(summ[8] != 0.0))
+        out = dict(com_start=summ[0:3].copy(), com_end=summ[3:6].copy(), horizontal_displacement=float(summ[6]),
+                   max_speed=float(summ[7]), diverged=bool(summ[8] != 0.0))
+        if dump is not None:
+            out["dump"] = dump
+        return out
 
     def evaluate_fitness(self, mat, wt, w, h, d, table=None, plane=None, sim=None) -> float:
         mat = np.ascontiguousarray(mat, np.uint8)

@@ -15,6 +15,7 @@ as data (``TrajectorySummary.diverged``, fitness 0).
 """
 from __future__ import annotations
 
+import math
 import ctypes as C
 import os
 from dataclasses import dataclass, field
@@ -239,6 +240,7 @@ def _declare(lib):
         "vx_batch_step": (i32, [vp, vp, P(SimConfig), i64, i64, vp]),
         "vx_batch_simulate": (i32, [vp, vp, P(SimConfig), vp]),
         "vx_batch_simulate_dev": (i32, [vp, vp, P(SimConfig), vp]),
+        "vx_batch_simulate_dump": (i32, [vp, vp, P(SimConfig), i32, i64, vp, vp, vp]),
         "vx_evaluate_dev": (i32, [vp, i32, i32, i32, i32, vp, vp, P(MaterialTable), P(GroundPlane), P(SimConfig), vp,
                                  i32, vp, vp]),
         "vx_evaluate": (i32, [vp, i32, i32, i32, i32, vp, vp, P(MaterialTable), P(GroundPlane), P(SimConfig), vp,
@@ -516,6 +518,20 @@ class Batch:
         out = (TrajectorySummary * max(1, len(self)))()
         _check(_lib().vx_batch_simulate(self.ctx.h, self.h, C.byref(sim), out), "simulate")
         return list(out)[:len(self)]
+
+    def simulate_dump(self, sim: SimConfig, stride: int):
+        """simulate(sys, cfg, &dump, stride) (physics.hpp:280-311) for every
+        robot: returns (summaries, dumps) with dumps[r] an (rows, 4) array of
+        TrajectorySample (t, com x, y, z).  The batch is unchanged."""
+        n = len(self)
+        n_steps = int(math.floor(sim.duration / sim.dt + 0.5)) if sim.dt > 0 else 0  # llround
+        cap = (-(-n_steps // stride) if stride > 0 else 0) + 1
+        rows = np.zeros((max(1, n), cap, 4))
+        counts = np.zeros(max(1, n), np.int64)
+        out = (TrajectorySummary * max(1, n))()
+        _check(_lib().vx_batch_simulate_dump(self.ctx.h, self.h, C.byref(sim), int(stride), cap, _ptr(rows),
+                                             _ptr(counts), out), "simulate_dump")
+        return list(out)[:n], [rows[r, :min(int(counts[r]), cap)].copy() for r in range(n)]
 
     def simulate_dev(self, sim: SimConfig, d_summaries: int):
         _check(_lib().vx_batch_simulate_dev(self.ctx.h, self.h, C.byref(sim), d_summaries), "simulate_dev")

@@ -1,5 +1,5 @@
-"""``python -m paper_2405_00698_b200 run.json [--resume checkpoint.json]``:
-run / resume an evolution from a reference run-config file (runner.main)."""
+"""``python -m paper_2405_00698_b200 {run,resume,bench,export-mesh} ...``:
+the reference CLI (voxevo_main.cpp) over this build (runner.main)."""
 import sys
 
 from .runner import main

@@ -145,6 +145,138 @@ vx_status simulate_impl(vx_ctx* ctx, vx_batch* b, const vx_sim* sim, int64_t k0,
     return VX_OK;
 }
 
+// center_of_mass (physics.hpp:265-277), one thread per robot walking its
+// masses in index order: the reference's sequential sums, bit for bit.
+__global__ void com_kernel(int n, const int64_t* __restrict__ mass_off, const int32_t* __restrict__ nmass,
+                           const double* __restrict__ pos, const double* __restrict__ mass, int64_t M,
+                           double* __restrict__ com) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    const int64_t o = mass_off[r];
+    double c0 = 0.0, c1 = 0.0, c2 = 0.0, total = 0.0;
+    for (int i = 0; i < nmass[r]; ++i) {
+        const double m = mass[o + i];
+        c0 += m * pos[o + i];
+        c1 += m * pos[M + o + i];
+        c2 += m * pos[2 * M + o + i];
+        total += m;
+    }
+    if (total > 0.0) {
+        c0 /= total;
+        c1 /= total;
+        c2 /= total;
+    }
+    com[3 * r] = c0;
+    com[3 * r + 1] = c1;
+    com[3 * r + 2] = c2;
+}
+
+// simulate() with its COM dump (physics.hpp:285-311): the integrator runs in
+// chunks of `stride` steps on the batch's own state (restored afterwards:
+// simulate takes the system by value), sampling the COM of every still-live
+// robot at each chunk start; a robot leaves the sampling at its first
+// diverged step (the fused kernels stop it there), like the reference's
+// break.  Chunked stepping is bit-identical to one launch (t = k*dt from the
+// global step index).
+vx_status simulate_dump_impl(vx_ctx* ctx, vx_batch* b, const vx_sim* sim, int32_t stride, int64_t cap,
+                             double* samples, int64_t* counts, vx_summary* h_out) {
+    const int n = b->n;
+    const int64_t n_steps = std::llround(sim->duration / sim->dt);  // physics.hpp:295
+    cudaStream_t s = ctx->stream;
+    const size_t sb = 3 * static_cast<size_t>(b->M) * sizeof(double);
+    DevBuf<double> save_pos, save_vel, d_com;
+    DevBuf<vx_summary> d_summ;
+    VX_TRY(save_pos.alloc(3 * b->M));
+    VX_TRY(save_vel.alloc(3 * b->M));
+    VX_TRY(d_com.alloc(3 * static_cast<size_t>(n)));
+    VX_TRY(d_summ.alloc(n));
+    VX_CUDA(cudaMemcpyAsync(save_pos.p, b->pos.p, sb, cudaMemcpyDeviceToDevice, s));
+    VX_CUDA(cudaMemcpyAsync(save_vel.p, b->vel.p, sb, cudaMemcpyDeviceToDevice, s));
+    std::vector<int32_t> nm(n);
+    VX_CUDA(cudaMemcpyAsync(nm.data(), b->nmass.p, n * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    std::vector<double> com(3 * static_cast<size_t>(n));
+    auto get_com = [&]() -> vx_status {
+        com_kernel<<<(n + 127) / 128, 128, 0, s>>>(n, b->mass_off.p, b->nmass.p, b->pos.p, b->mass.p, b->M, d_com.p);
+        VX_CUDA(cudaGetLastError());
+        VX_CUDA(cudaMemcpyAsync(com.data(), d_com.p, com.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
+        VX_CUDA(cudaStreamSynchronize(s));
+        return VX_OK;
+    };
+    std::vector<vx_summary> acc(n), part(n);
+    std::vector<uint8_t> live(n);
+    std::vector<double> max_speed(n, 0.0);
+    for (int r = 0; r < n; ++r) {
+        std::memset(&acc[r], 0, sizeof(vx_summary));
+        counts[r] = 0;
+        live[r] = nm[r] > 0;  // an empty system returns the default summary, no samples (:291)
+    }
+    auto push = [&](int r, double t) {
+        if (counts[r] < cap) {
+            double* row = samples + (static_cast<size_t>(r) * cap + counts[r]) * 4;
+            row[0] = t;
+            row[1] = com[3 * r];
+            row[2] = com[3 * r + 1];
+            row[3] = com[3 * r + 2];
+        }
+        ++counts[r];
+    };
+    vx_status st = get_com();
+    if (st != VX_OK) return st;
+    for (int r = 0; r < n; ++r)
+        if (nm[r] > 0)
+            for (int c = 0; c < 3; ++c) acc[r].com_start[c] = com[3 * r + c];
+    const int64_t chunk = stride > 0 ? stride : std::max<int64_t>(1, n_steps);
+    for (int64_t k = 0; k < n_steps && st == VX_OK; k += chunk) {
+        if (stride > 0) {
+            if (k > 0) st = get_com();
+            if (st != VX_OK) break;
+            for (int r = 0; r < n; ++r)
+                if (live[r]) push(r, static_cast<double>(k) * sim->dt);
+        }
+        const int64_t len = std::min(chunk, n_steps - k);
+        st = integrate(ctx, b, sim, k, len, true, nullptr, 0, d_summ.p, nullptr);
+        if (st != VX_OK) break;
+        VX_CUDA(cudaMemcpyAsync(part.data(), d_summ.p, n * sizeof(vx_summary), cudaMemcpyDeviceToHost, s));
+        VX_CUDA(cudaStreamSynchronize(s));
+        bool any = false;
+        for (int r = 0; r < n; ++r) {
+            if (!live[r]) continue;
+            acc[r].steps += part[r].steps;
+            acc[r].spring_updates += part[r].spring_updates;
+            if (part[r].max_speed > max_speed[r]) max_speed[r] = part[r].max_speed;
+            for (int c = 0; c < 3; ++c) acc[r].com_end[c] = part[r].com_end[c];
+            if (part[r].diverged) {
+                acc[r].diverged = 1;
+                live[r] = 0;
+            }
+            any = any || live[r];
+        }
+        if (!any) break;
+    }
+    if (st == VX_OK) {
+        // final sample at t = n_steps*dt and the summary (:303-309); a robot
+        // that diverged keeps the state of its diverging step (com_end of
+        // that chunk), everyone else the final state
+        for (int r = 0; r < n; ++r) {
+            if (nm[r] <= 0) continue;
+            if (n_steps == 0)
+                for (int c = 0; c < 3; ++c) acc[r].com_end[c] = acc[r].com_start[c];
+            for (int c = 0; c < 3; ++c) com[3 * r + c] = acc[r].com_end[c];
+            push(r, static_cast<double>(n_steps) * sim->dt);
+            const double dx = acc[r].com_end[0] - acc[r].com_start[0];
+            const double dy = acc[r].com_end[1] - acc[r].com_start[1];
+            acc[r].horizontal_displacement = std::sqrt(dx * dx + dy * dy);
+            acc[r].max_speed = max_speed[r];
+        }
+        if (h_out) std::memcpy(h_out, acc.data(), n * sizeof(vx_summary));
+    }
+    // simulate() never modifies the caller's system
+    VX_CUDA(cudaMemcpyAsync(b->pos.p, save_pos.p, sb, cudaMemcpyDeviceToDevice, s));
+    VX_CUDA(cudaMemcpyAsync(b->vel.p, save_vel.p, sb, cudaMemcpyDeviceToDevice, s));
+    VX_CUDA(cudaStreamSynchronize(s));
+    return st;
+}
+
 }  // namespace
 
 extern "C" {
@@ -445,6 +577,16 @@ vx_status vx_batch_simulate(vx_ctx* ctx, vx_batch* b, const vx_sim* sim, vx_summ
     if (!sim) return VX_EINVAL;
     const int64_t n_steps = std::llround(sim->duration / sim->dt);  // physics.hpp:295
     return simulate_impl(ctx, b, sim, 0, n_steps, false, summaries, nullptr);
+}
+
+vx_status vx_batch_simulate_dump(vx_ctx* ctx, vx_batch* b, const vx_sim* sim, int32_t stride, int64_t cap,
+                                 double* samples, int64_t* counts, vx_summary* summaries) {
+    if (!ctx || !b || !sim || cap < 0 || (cap > 0 && !samples) || !counts) return VX_EINVAL;
+    if (!(sim->dt > 0.0)) return (set_error("SimConfig: dt must be > 0"), VX_EINVAL);
+    if (!(sim->duration >= 0.0)) return (set_error("SimConfig: duration must be >= 0"), VX_EINVAL);
+    if (!(sim->actuation_frequency > 0.0)) return (set_error("SimConfig: frequency must be > 0"), VX_EINVAL);
+    if (b->n <= 0) return VX_OK;
+    return simulate_dump_impl(ctx, b, sim, stride, cap, samples, counts, summaries);
 }
 
 vx_status vx_batch_simulate_dev(vx_ctx* ctx, vx_batch* b, const vx_sim* sim, vx_summary* d_summaries) {

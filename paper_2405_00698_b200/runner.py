@@ -139,21 +139,170 @@ def resume_run(checkpoint_path: str, rc: RunConfig, ctx: Optional[Context] = Non
     return run_loop(load_run(checkpoint_path, ctx), rc, log)
 
 
-def main(argv=None) -> int:
-    """``python -m paper_2405_00698_b200 run.json [--resume checkpoint.json]``:
-    the reference CLI's run / resume over this build (voxevo_main.cpp)."""
-    import argparse
+def _fmt_g(x: float) -> str:
+    """std::ostream's default double format (precision 6, %g)."""
+    return "%g" % x
+
+
+def print_summary(st: EvolutionState, rc: RunConfig, out: TextIO = sys.stdout):
+    """print_summary (voxevo_main.cpp:43-50)."""
+    paths = artifact_paths(rc.out_dir)
+    best_f, best_p = st.best()
+    out.write("done: %d generations, best fitness %s m\n" % (len(st.history), _fmt_g(best_f)))
+    out.write("  curves:     %s\n" % paths.curves)
+    out.write("  checkpoint: %s\n" % paths.checkpoint)
+    if best_p is not None:
+        out.write("  champion:   %s\n" % paths.best_genome)
+
+
+def _add_overrides(cmd, with_population=True):
+    """CommonOverrides::add_to (voxevo_main.cpp:23-32)."""
+    cmd.add_argument("--seed", type=int)
+    cmd.add_argument("--generations", type=int)
+    if with_population:
+        cmd.add_argument("--population", type=int)
+    cmd.add_argument("--threads", type=int)
+    cmd.add_argument("--advisor", choices=["off", "scripted", "llm", "replay"])
+    cmd.add_argument("--out", dest="out_dir")
+
+
+def cmd_run(a) -> int:
+    """cmd_run (voxevo_main.cpp:52-60): defaults, then the config file, then flags."""
     from .serialize import load_run_config
-    ap = argparse.ArgumentParser(prog="python -m paper_2405_00698_b200")
-    ap.add_argument("config")
-    ap.add_argument("--resume", default=None)
-    a = ap.parse_args(argv)
-    rc = load_run_config(a.config)
-    if a.resume:
-        resume_run(a.resume, rc, log=sys.stdout)
-    else:
-        start_run(rc, log=sys.stdout)
+    rc = load_run_config(a.config) if a.config else RunConfig()
+    e = rc.evolution
+    if a.seed is not None:
+        e.seed = a.seed
+    if a.generations is not None:
+        e.generations = a.generations
+    if a.population is not None:
+        e.population = a.population
+    if a.threads is not None:
+        e.threads = a.threads
+    if a.advisor is not None:
+        rc.advisor = a.advisor
+    if a.out_dir is not None:
+        rc.out_dir = a.out_dir
+    st = start_run(rc, log=sys.stdout)
+    print_summary(st, rc)
     return 0
+
+
+def cmd_resume(a) -> int:
+    """cmd_resume (voxevo_main.cpp:62-77): search settings stay with the
+    checkpoint unless a flag overrides them."""
+    from .serialize import load_run_config
+    rc = load_run_config(a.config) if a.config else RunConfig()
+    st = load_run(a.checkpoint)
+    if a.generations is not None:
+        st.config.generations = a.generations
+    if a.threads is not None:
+        st.config.threads = a.threads
+    if a.advisor is not None:
+        rc.advisor = a.advisor
+    if a.out_dir is not None:
+        rc.out_dir = a.out_dir
+    st = run_loop(st, rc, sys.stdout)
+    print_summary(st, rc)
+    return 0
+
+
+def cmd_bench(a) -> int:
+    """cmd_bench (voxevo_main.cpp:79-101) over the device run_bench: the same
+    line with the device in place of the worker-thread count."""
+    from . import run_bench
+    r = run_bench(a.jobs, a.steps, a.grid, a.dt)
+    sys.stdout.write("device %2d: %d steps x %d jobs, %d springs/robot -> %d updates in %.3fs (%.3g/s)%s\n"
+                     % (0, a.steps, a.jobs, r["springs_per_robot"], r["spring_updates"], r["seconds"],
+                        r["updates_per_second"], "  [DIVERGED]" if r["diverged"] else ""))
+    if r["spring_updates"] != r["expected_updates"]:
+        sys.stderr.write("update count mismatch: expected %d\n" % r["expected_updates"])
+        return 1
+    if a.compare_single:
+        sys.stderr.write("--compare-single: the device path has no worker-thread count; "
+                         "bench.py --impl reference times the reference CPU build\n")
+    return 0
+
+
+def cmd_export(a) -> int:
+    """cmd_export (voxevo_main.cpp:103-126): decode (and keep the largest
+    component unless --full) on the device, then the reference's formats."""
+    from . import decode, largest_component
+    from .export import export_mesh_obj, export_voxel_listing
+    from .serialize import load_genome
+    params, bmat, arch = load_genome(a.genome)
+    w, h, d = a.grid
+    mats, wts = decode(params[None], bmat[None], arch, w, h, d)
+    if not a.full:
+        mats = largest_component(mats, w, h, d)
+    occupied = int((mats[0] != 0).sum())
+    if occupied == 0:
+        sys.stderr.write("genome decodes to an empty robot at %dx%dx%d\n" % (w, h, d))
+        return 1
+    if a.out:
+        export_mesh_obj(a.out, mats[0], w, h, d, a.edge)
+        sys.stdout.write("mesh:   %s\n" % a.out)
+    if a.voxels:
+        export_voxel_listing(a.voxels, mats[0], wts[0], w, h, d)
+        sys.stdout.write("voxels: %s\n" % a.voxels)
+    sys.stdout.write("voxels occupied: %d\n" % occupied)
+    return 0
+
+
+def main(argv=None) -> int:
+    """The reference CLI (voxevo_main.cpp:130-190) over this build:
+
+      python -m paper_2405_00698_b200 run [--config c.json] [--seed --generations --population --threads
+                                           --advisor --out]
+      python -m paper_2405_00698_b200 resume --checkpoint ck.json [--config c.json] [--generations --threads
+                                              --advisor --out]
+      python -m paper_2405_00698_b200 bench [--jobs 16 --steps 2000 --grid 4 --dt 1e-5 --threads N
+                                             --compare-single]
+      python -m paper_2405_00698_b200 export-mesh --genome g.json [--out robot.obj --voxels v.txt
+                                                   --grid W H D --full --edge 0.1]
+
+    Errors print ``error: <what>`` and exit 1, like the reference's catch-all."""
+    import argparse
+    from . import MaterialTable, VoxevoError
+    from .export import ExportError
+    from .serialize import CheckpointError, ConfigError
+    ap = argparse.ArgumentParser(prog="python -m paper_2405_00698_b200",
+                                 description="voxevo: evolve simulated soft voxel robots")
+    sub = ap.add_subparsers(dest="cmd", required=True)
+    run = sub.add_parser("run", help="Start an evolution run")
+    run.add_argument("--config")
+    _add_overrides(run)
+    res = sub.add_parser("resume", help="Continue from a checkpoint")
+    res.add_argument("--checkpoint", required=True)
+    res.add_argument("--config")
+    _add_overrides(res, with_population=False)
+    res.set_defaults(seed=None)
+    ben = sub.add_parser("bench", help="Measure simulator throughput")
+    ben.add_argument("--jobs", type=int, default=16)
+    ben.add_argument("--steps", type=int, default=2000)
+    ben.add_argument("--threads", type=int, default=1)
+    ben.add_argument("--grid", type=int, default=4)
+    ben.add_argument("--dt", type=float, default=1e-5)
+    ben.add_argument("--compare-single", action="store_true")
+    exp = sub.add_parser("export-mesh", help="Write a genome's morphology as OBJ")
+    exp.add_argument("--genome", required=True)
+    exp.add_argument("--out", default="robot.obj")
+    exp.add_argument("--voxels", default="")
+    exp.add_argument("--grid", type=int, nargs=3, default=[5, 5, 5])
+    exp.add_argument("--full", action="store_true")
+    exp.add_argument("--edge", type=float, default=MaterialTable().voxel_edge)
+    a = ap.parse_args(argv)
+    for name in ("jobs", "steps", "threads", "grid"):
+        if a.cmd == "bench" and getattr(a, name) <= 0:
+            ap.error("--%s must be positive" % name)
+    for path in (getattr(a, "config", None), getattr(a, "checkpoint", None), getattr(a, "genome", None)):
+        if path and not os.path.isfile(path):
+            ap.error("file does not exist: %s" % path)
+    try:
+        return {"run": cmd_run, "resume": cmd_resume, "bench": cmd_bench, "export-mesh": cmd_export}[a.cmd](a)
+    except (VoxevoError, CheckpointError, ConfigError, ExportError, ValueError, OSError) as e:
+        sys.stderr.write("error: %s\n" % e)
+        return 1
 
 
 if __name__ == "__main__":

@@ -568,9 +568,28 @@ def save_genome(path: str, params: np.ndarray, bmat: np.ndarray, arch: Arch):
     save_json_file(path, wrap_payload("genome", genome_to_json(params, bmat, arch)))
 
 
-def load_genome(path: str, arch: Arch) -> tuple:
-    """load_genome (serialize.hpp:319-321) -> (flat params, b_matrix)."""
-    return genome_from_json(unwrap_payload(load_json_file(path), "genome"), arch)
+def genome_arch(j: dict) -> Arch:
+    """The architecture a genome JSON declares (encoding m / sigma, hidden
+    layer widths) — what the reference's self-describing Genome carries."""
+    enc = _at(j, "encoding")
+    sigma = float(enc["sigma"]) if isinstance(enc, dict) and "sigma" in enc else 1.0
+    widths = [_int(lj, "out") for lj in _at(j, "hidden")]
+    try:
+        return Arch.make(_int(enc, "m"), widths, sigma)
+    except ValueError as e:
+        raise CheckpointError(str(e)) from e
+
+
+def load_genome(path: str, arch: Optional[Arch] = None) -> tuple:
+    """load_genome (serialize.hpp:319-321) -> (flat params, b_matrix); with
+    ``arch=None`` the architecture is read from the file and returned too:
+    (flat params, b_matrix, arch)."""
+    j = unwrap_payload(load_json_file(path), "genome")
+    if arch is None:
+        a = genome_arch(j)
+        p, b = genome_from_json(j, a)
+        return p, b, a
+    return genome_from_json(j, arch)
 
 
 def curves_csv(history: list) -> str:
