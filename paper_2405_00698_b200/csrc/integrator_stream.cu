@@ -20,6 +20,7 @@
 // 24 B force load (+ 48 B neighbour state when the state is off chip): it is
 // L2/HBM-bandwidth bound by design (bench/scale numbers in profiles/).
 // Compiled with --fmad=false.
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 #include <string>
@@ -459,7 +460,7 @@ struct SymGeom {
 };
 
 struct SymLayout {
-    size_t per_robot, k, r0, vox, x0, x1, mc, mask, cph, sph, sa;
+    size_t per_robot, k, r0, vox, x0, x1, mc, mask, cph, sph, sa, amap;
 };
 
 template <int N>
@@ -482,6 +483,7 @@ SymLayout sym_layout() {
     L.cph = take((G::NCELL + 1) * 8ull);
     L.sph = take((G::NCELL + 1) * 8ull);
     L.sa = take((G::NCELL + 1) * 8ull);
+    L.amap = take((G::NCELL + 2) * 4ull);  // voxel -> actuator id, then [NCELL + 1] = table size
     L.per_robot = o;
     return L;
 }
@@ -501,6 +503,7 @@ struct SymArgs {
     SymLayout L;
     double zero_len2;
     double zeta2, mu;
+    int32_t* ntab_max;  // prep: max actuator-table size over the batch
 };
 
 template <int N>
@@ -521,18 +524,62 @@ __global__ void __launch_bounds__(1024) stream_sym_prep_kernel(SymArgs A) {
     double* CPH = at<double>(base, L.cph);
     double* SPH = at<double>(base, L.sph);
     double* SAG = at<double>(base, L.sa);
+    int32_t* AMAP = at<int32_t>(base, L.amap);
     const int64_t mo = b.mass_off[r], so = b.spring_off[r];
     const int nm = b.nmass[r], ns = b.nspring[r];
-    for (int v = threadIdx.x; v <= G::NCELL; v += blockDim.x) {
-        CPH[v] = 1.0;
-        SPH[v] = 0.0;
-        SAG[v] = 0.0;
+    // compact actuator tables: only the voxels that actuate a spring get a
+    // row (ids in voxel order), the last row is the passive sentinel (sin 0,
+    // cos 1, amplitude 0: rest = r0 + (0 * r0) * D = r0).  The kernel keeps
+    // the drive and amplitude tables in shared memory, and the smaller they
+    // are the more of the SM's unified L1 serves the neighbour reads.
+#ifndef VX_SYM_COMPACT
+#define VX_SYM_COMPACT 1
+#endif
+    for (int v = threadIdx.x; v < G::NCELL; v += blockDim.x) AMAP[v] = VX_SYM_COMPACT ? 0 : 1;
+    __syncthreads();
+    for (int s = threadIdx.x; s < ns && VX_SYM_COMPACT; s += blockDim.x) {
+        const int v = A.act_vox[so + s];
+        if (v >= 0) AMAP[v] = 1;
+    }
+    __syncthreads();
+    {  // exclusive scan of the flags over NCELL voxels, 1024 threads x contiguous runs
+        __shared__ int s_cnt[1024];
+        constexpr int RUN = (G::NCELL + 1023) / 1024;
+        const int lo = threadIdx.x * RUN, hi = min(G::NCELL, lo + RUN);
+        int c = 0;
+        for (int v = lo; v < hi; ++v) c += AMAP[v];
+        s_cnt[threadIdx.x] = c;
+        __syncthreads();
+        for (int o = 1; o < 1024; o <<= 1) {  // Hillis-Steele inclusive scan
+            const int add = threadIdx.x >= o ? s_cnt[threadIdx.x - o] : 0;
+            __syncthreads();
+            s_cnt[threadIdx.x] += add;
+            __syncthreads();
+        }
+        int id = s_cnt[threadIdx.x] - c;
+        for (int v = lo; v < hi; ++v) {
+            const int f = AMAP[v];
+            AMAP[v] = f ? id : -1;
+            id += f;
+        }
+        if (threadIdx.x == 1023) {
+            AMAP[G::NCELL] = s_cnt[1023];           // sentinel id
+            AMAP[G::NCELL + 1] = s_cnt[1023] + 1;   // table size
+            atomicMax(A.ntab_max, s_cnt[1023] + 1);
+        }
+    }
+    __syncthreads();
+    const int sentinel = AMAP[G::NCELL];
+    if (threadIdx.x == 0) {
+        CPH[sentinel] = 1.0;
+        SPH[sentinel] = 0.0;
+        SAG[sentinel] = 0.0;
     }
     for (int k = threadIdx.x; k < PCOL; k += blockDim.x)
         for (int d = 0; d < 13; ++d) {
             K[d * PCOL + k] = 1.0;
             R0[d * PCOL + k] = 1.0;
-            VOX[d * PCOL + k] = static_cast<uint16_t>(G::NCELL);
+            VOX[d * PCOL + k] = static_cast<uint16_t>(sentinel);
         }
     for (int k = threadIdx.x; k < NVP; k += blockDim.x) {
         MASK[k] = 0u;
@@ -544,9 +591,10 @@ __global__ void __launch_bounds__(1024) stream_sym_prep_kernel(SymArgs A) {
     for (int s = threadIdx.x; s < ns; s += blockDim.x) {
         const int v = A.act_vox[so + s];
         if (v >= 0) {
-            CPH[v] = b.cosph[so + s];
-            SPH[v] = b.sinph[so + s];
-            SAG[v] = A.sign[so + s] * A.amp[so + s];  // sign * amplitude (physics.hpp:153)
+            const int id = AMAP[v];
+            CPH[id] = b.cosph[so + s];
+            SPH[id] = b.sinph[so + s];
+            SAG[id] = A.sign[so + s] * A.amp[so + s];  // sign * amplitude (physics.hpp:153)
         }
     }
     for (int m = threadIdx.x; m < nm; m += blockDim.x) {
@@ -577,7 +625,7 @@ __global__ void __launch_bounds__(1024) stream_sym_prep_kernel(SymArgs A) {
                 K[d * PCOL + key] = b.k[so + sp];
                 R0[d * PCOL + key] = b.rest0[so + sp];
                 const int av = A.act_vox[so + sp];
-                VOX[d * PCOL + key] = static_cast<uint16_t>(av >= 0 ? av : G::NCELL);
+                VOX[d * PCOL + key] = static_cast<uint16_t>(av >= 0 ? AMAP[av] : sentinel);
             } else {
                 fmask |= 1u << d;
             }
@@ -586,16 +634,25 @@ __global__ void __launch_bounds__(1024) stream_sym_prep_kernel(SymArgs A) {
     }
 }
 
+// The per-actuator drive table D is single-buffered (a second barrier per
+// step rewrites it) unless VX_SYM_DBUF: shared memory taken by tables is L1
+// the neighbour state / forward-slot reads do not get.
+#ifndef VX_SYM_DBUF
+#define VX_SYM_DBUF 0
+#endif
+constexpr int kSymDBuf = VX_SYM_DBUF ? 2 : 1;
+
 template <int N>
 __global__ void __launch_bounds__(kStreamThreads, 1) stream_sym_kernel(SymArgs A) {
     using G = SymGeom<N>;
     constexpr int PCOL = G::PC, NVP = G::NVP, XS = G::XS, PAD = G::PAD, VW = G::VW, T = G::T, MPT = G::MPT;
-    constexpr int NV = G::NV, NT = G::NCELL + 1;
+    constexpr int NV = G::NV;
     const int r = blockIdx.x;
     const BatchView& b = A.b;
     const SymLayout& L = A.L;
     const int t = threadIdx.x;
     unsigned char* base = A.scratch + static_cast<size_t>(r) * L.per_robot;
+    const int NT = at<int32_t>(base, L.amap)[G::NCELL + 1];  // this robot's actuator rows + sentinel
     const double* __restrict__ K = at<double>(base, L.k);
     const double* __restrict__ R0 = at<double>(base, L.r0);
     const uint16_t* __restrict__ VOX = at<uint16_t>(base, L.vox);
@@ -611,8 +668,8 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_sym_kernel(SymArgs A
     vx_summary* out = A.out ? A.out + r : nullptr;
 
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    double* D = reinterpret_cast<double*>(smem_raw);  // [2][NT] drive per voxel (double-buffered)
-    double* SA = D + 2 * NT;                           // [NT]
+    double* D = reinterpret_cast<double*>(smem_raw);  // [kSymDBuf][NT] drive per actuator row
+    double* SA = D + kSymDBuf * NT;                    // [NT]
     __shared__ double s_maxsq[32];
 
     if (nm == 0) {
@@ -662,7 +719,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_sym_kernel(SymArgs A
     int64_t steps = 0, ok_phase1 = 0;
     int diverged = 0;
     for (int64_t kstep = 0; kstep < A.n_steps; ++kstep) {
-        const double* Dc = D + (kstep & 1) * NT;
+        const double* Dc = D + (kSymDBuf == 2 ? (kstep & 1) * NT : 0);
         int zero_len = 0, bad = 0;
         double step_max = 0.0;
         for (int j = 0; j < MPT; ++j) {
@@ -787,12 +844,17 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_sym_kernel(SymArgs A
                 !(fabs(pz) <= kDivergenceBound))
                 bad = 1;
         }
-        if (kstep + 1 < A.n_steps) {  // next drive into the other buffer
+        if (kSymDBuf == 2 && kstep + 1 < A.n_steps) {  // next drive into the other buffer
             const double2 drv = __ldg(A.drive + kstep + 1);
             double* Dn = D + ((kstep + 1) & 1) * NT;
             for (int v = t; v < NT; v += T) Dn[v] = drv.x * CPH[v] + drv.y * SPH[v];
         }
         const int flags = __syncthreads_or(zero_len | (bad << 1));
+        if (kSymDBuf == 1 && !(flags & 3) && kstep + 1 < A.n_steps) {  // every read of D[k] is behind the barrier
+            const double2 drv = __ldg(A.drive + kstep + 1);
+            for (int v = t; v < NT; v += T) D[v] = drv.x * CPH[v] + drv.y * SPH[v];
+            __syncthreads();
+        }
         ++steps;
         if (flags & 1) {  // step() returned before touching any mass: keep X[k]
             diverged = 1;
@@ -863,10 +925,16 @@ vx_status launch_stream_sym(vx_ctx* ctx, vx_batch* b, const StreamArgs& S) {
     A.L = sym_layout<N>();
     VX_TRY(ctx->stream_scratch.alloc(A.L.per_robot * static_cast<size_t>(b->n)));
     A.scratch = ctx->stream_scratch.p;
+    VX_TRY(ctx->stream_ntab.alloc(1));
+    VX_CUDA(cudaMemsetAsync(ctx->stream_ntab.p, 0, sizeof(int32_t), ctx->stream));
+    A.ntab_max = ctx->stream_ntab.p;
     stream_sym_prep_kernel<N><<<b->n, 1024, 0, ctx->stream>>>(A);
     ctx->launches++;
     VX_CUDA(cudaGetLastError());
-    const size_t smem = 3ull * (SymGeom<N>::NCELL + 1) * sizeof(double);
+    int32_t ntab = 0;  // shared memory sized for the batch's largest actuator table
+    VX_CUDA(cudaMemcpyAsync(&ntab, ctx->stream_ntab.p, sizeof(int32_t), cudaMemcpyDeviceToHost, ctx->stream));
+    VX_CUDA(cudaStreamSynchronize(ctx->stream));
+    const size_t smem = (kSymDBuf + 1ull) * std::max(1, ntab) * sizeof(double);
     VX_CUDA(cudaFuncSetAttribute(stream_sym_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(smem)));
     stream_sym_kernel<N><<<b->n, kStreamThreads, smem, ctx->stream>>>(A);
