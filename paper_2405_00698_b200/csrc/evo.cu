@@ -403,9 +403,14 @@ vx_status vx_evo_finish(vx_evo* e, vx_report* rep) {
     if (!e->h_masks.empty())
         VX_CUDA(cudaMemcpyAsync(e->d_masks.p, e->h_masks.data(), e->h_masks.size() * sizeof(uint32_t),
                                 cudaMemcpyHostToDevice, ctx->stream));
-    for (size_t j = 0; j < e->h_mut.chunks(); ++j)  // pinned chunks: true async copies
-        VX_CUDA(cudaMemcpyAsync(e->d_mut.p + j * MutStore::kChunk, e->h_mut.chunk(j),
-                                e->h_mut.chunk_size(j) * sizeof(MutEntry), cudaMemcpyHostToDevice, ctx->stream));
+    for (size_t j = 0, nch = e->h_mut.chunks(); j < nch;) {  // pinned chunks: true async copies, one per run
+        size_t k = j + 1;                                      // of chunks in one pinned slab
+        while (k < nch && e->h_mut.continues(k)) ++k;
+        const size_t count = (k - 1 - j) * MutStore::kChunk + e->h_mut.chunk_size(k - 1);
+        VX_CUDA(cudaMemcpyAsync(e->d_mut.p + j * MutStore::kChunk, e->h_mut.chunk(j), count * sizeof(MutEntry),
+                                cudaMemcpyHostToDevice, ctx->stream));
+        j = k;
+    }
     if (!e->mut_uploaded) VX_CUDA(cudaEventCreateWithFlags(&e->mut_uploaded, cudaEventDisableTiming));
     VX_CUDA(cudaEventRecord(e->mut_uploaded, ctx->stream));
     BreedArgs A{};

@@ -224,23 +224,30 @@ struct MutWriter {
             pool.cv.notify_one();
         }
     }
-    void grow() {
-        void* p = st.alloc_ ? st.alloc_(MutStore::kChunk * sizeof(MutEntry))
-                            : ::operator new(MutStore::kChunk * sizeof(MutEntry));
+    void grow() {  // a slab as large as everything so far (1..256 chunks): few, large pinned allocations
+        const size_t n = std::min<size_t>(256, std::max<size_t>(1, st.e_.size()));
+        const size_t bytes = n * MutStore::kChunk * sizeof(MutEntry);
+        void* p = st.alloc_ ? st.alloc_(bytes) : ::operator new(bytes, std::nothrow);
         if (!p) throw std::bad_alloc();
-        st.e_.push_back(static_cast<MutEntry*>(p));
-        st.r2_.push_back(new uint64_t[MutStore::kChunk]);
+        st.slabs_.push_back(p);
+        uint64_t* r2 = new uint64_t[n * MutStore::kChunk];
+        st.r2_slabs_.push_back(r2);
+        for (size_t c = 0; c < n; ++c) {
+            st.e_.push_back(static_cast<MutEntry*>(p) + c * MutStore::kChunk);
+            st.r2_.push_back(r2 + c * MutStore::kChunk);
+            st.slab_of_.push_back(static_cast<uint32_t>(st.slabs_.size() - 1));
+        }
     }
 };
 
 MutStore::~MutStore() {
-    for (MutEntry* p : e_) {
+    for (void* p : slabs_) {
         if (free_)
             free_(p);
         else
             ::operator delete(p);
     }
-    for (uint64_t* p : r2_) delete[] p;
+    for (uint64_t* p : r2_slabs_) delete[] p;
 }
 
 void MutStore::flatten(std::vector<MutEntry>& out) const {

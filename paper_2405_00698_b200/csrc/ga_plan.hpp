@@ -55,13 +55,18 @@ public:
     size_t chunks() const { return (n_ + kChunk - 1) / kChunk; }
     const MutEntry* chunk(size_t j) const { return e_[j]; }
     size_t chunk_size(size_t j) const { return std::min(kChunk, n_ - j * kChunk); }
+    // chunk j continues chunk j-1 inside the same allocation (one copy may span both)
+    bool continues(size_t j) const { return j > 0 && slab_of_[j] == slab_of_[j - 1]; }
     void flatten(std::vector<MutEntry>& out) const;
     void clear() { n_ = 0; }
 
 private:
     friend struct MutWriter;
-    std::vector<MutEntry*> e_;  // delta holds the first raw word until its normal is computed
+    std::vector<MutEntry*> e_;  // per chunk; delta holds the first raw word until its normal is computed
     std::vector<uint64_t*> r2_;
+    std::vector<void*> slabs_;           // e_ chunks come in slabs (geometric growth, few pinned allocations)
+    std::vector<uint64_t*> r2_slabs_;
+    std::vector<uint32_t> slab_of_;
     size_t n_ = 0;
     AllocFn alloc_;
     FreeFn free_;
