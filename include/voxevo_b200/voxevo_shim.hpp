@@ -16,6 +16,8 @@
 #pragma once
 
 #include <optional>
+#include <algorithm>
+#include <cmath>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -202,8 +204,11 @@ inline MassSpringSystem build_mass_spring(const VoxelGrid& grid, const MaterialT
     return sys;
 }
 
-// simulate (physics.hpp:287-311); the system is taken by value like the reference's.
-inline TrajectorySummary simulate(const MassSpringSystem& sys, const SimConfig& cfg, Device& dev = default_device()) {
+// simulate (physics.hpp:280-311), including the optional COM dump every
+// `stride` steps; the system is taken by value like the reference's.
+inline TrajectorySummary simulate(const MassSpringSystem& sys, const SimConfig& cfg,
+                                  std::vector<TrajectorySample>* dump = nullptr, int stride = 0,
+                                  Device& dev = default_device()) {
     cfg.validate();
     TrajectorySummary out;
     if (sys.masses.empty()) return out;
@@ -237,7 +242,18 @@ inline TrajectorySummary simulate(const MassSpringSystem& sys, const SimConfig& 
                           rest0.data(), zeta.data(), act.data(), sign.data(), amp.data(), phase.data(), &p, &b));
     const vx_sim s = to_c(cfg);
     vx_summary sum{};
-    const vx_status st = vx_batch_simulate(dev.get(), b, &s, &sum);
+    vx_status st;
+    if (dump) {
+        const long long n_steps = std::llround(cfg.duration / cfg.dt);
+        const int64_t cap = (stride > 0 ? (n_steps + stride - 1) / stride : 0) + 1;
+        std::vector<double> rows(4 * static_cast<size_t>(cap));
+        int64_t count = 0;
+        st = vx_batch_simulate_dump(dev.get(), b, &s, stride, cap, rows.data(), &count, &sum);
+        for (int64_t q = 0; st == VX_OK && q < std::min(count, cap); ++q)
+            dump->push_back({rows[4 * q], {rows[4 * q + 1], rows[4 * q + 2], rows[4 * q + 3]}});
+    } else {
+        st = vx_batch_simulate(dev.get(), b, &s, &sum);
+    }
     vx_batch_free(b);
     check(st);
     out.com_start = {sum.com_start[0], sum.com_start[1], sum.com_start[2]};

@@ -63,6 +63,19 @@ int main() {
     report("simulate 1000 steps: displacement rel <= 1e-3", rel <= 1e-3 && rs.diverged == gs.diverged,
            "ref " + std::to_string(rs.horizontal_displacement) + " rel " + std::to_string(rel));
 
+    // simulate with the COM dump (physics.hpp:285-311): same sample times, COMs within the chaos floor
+    std::vector<TrajectorySample> rd, gd;
+    simulate(sys, sim, &rd, 300);
+    b200::simulate(sys, sim, &gd, 300);
+    bool dump_ok = rd.size() == gd.size();
+    for (size_t q = 0; dump_ok && q < rd.size(); ++q) {
+        dump_ok = rd[q].t == gd[q].t;
+        for (int c = 0; c < 3; ++c)
+            dump_ok = dump_ok && std::abs(rd[q].com[c] - gd[q].com[c]) <= 1e-9 + 1e-6 * std::abs(rd[q].com[c]);
+    }
+    report("simulate with dump every 300 steps: rows and times match", dump_ok,
+           std::to_string(rd.size()) + " rows");
+
     // desk GA (acceptance_main.cpp:193-211 shape): reference genomes on the
     // GPU; draw consumption is fitness-independent -> identical RNG streams
     EvolutionConfig cfg;
