@@ -7,6 +7,8 @@ that do not divide the horizon."""
 import numpy as np
 import pytest
 
+import oracle
+
 pytestmark = pytest.mark.gpu
 
 KERNEL = {4: "lattice", 6: "lattice", 10: "cluster", 20: "stream"}
@@ -70,3 +72,23 @@ def test_simulate_dump_divergence(vx, ctx, orc):
     summ, dumps = _check(vx, ctx, orc, n, items, vx.SimConfig(duration=600 * 1e-5), 100, mutate)
     assert summ[1].diverged and not summ[0].diverged
     assert len(dumps[1]) < len(dumps[0])
+
+
+def test_simulate_dump_uploaded_systems(vx, ctx, orc):
+    """Host-assembled systems run the generic integrator; the dump follows the
+    same rows, bit for bit (phases overridden with glibc's, as the reference
+    computes them)."""
+    n = 4
+    items = _systems(vx, ctx, orc, n, 2, 3)
+    systems = [orc.build(m, w, n, n, n) for m, w in items] + [oracle.dumbbell(0.2, 100.0, 0.1, 0.15)]
+    batch = vx.upload_systems(systems, ctx=ctx)
+    batch.override_phase(np.concatenate([orc.workspace(s)["sin_phase"] for s in systems]),
+                         np.concatenate([orc.workspace(s)["cos_phase"] for s in systems]))
+    sim = vx.SimConfig(duration=700 * 1e-5)
+    summ, dumps = batch.simulate_dump(sim, 64)
+    assert ctx.last_integrator == "generic"
+    for r, s in enumerate(systems):
+        ref = orc.simulate(s, sim.as_array(), stride=64)
+        np.testing.assert_array_equal(dumps[r], ref["dump"])
+        assert summ[r].horizontal_displacement == ref["horizontal_displacement"]
+        assert summ[r].max_speed == ref["max_speed"]
