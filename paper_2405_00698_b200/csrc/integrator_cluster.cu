@@ -33,6 +33,7 @@
 #include <string>
 #include <type_traits>
 
+#include "vx_cluster.cuh"
 #include "vx_internal.cuh"
 
 namespace vx {
@@ -62,35 +63,6 @@ struct ClArgs {
     int vw, vh, ncell;
     double zero_len2;
 };
-
-__device__ __forceinline__ uint32_t smem_addr(const void* p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ uint32_t map_rank(uint32_t addr, uint32_t rank) {
-    uint32_t r;
-    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
-    return r;
-}
-__device__ __forceinline__ void st_remote(uint32_t addr, double v) {
-    asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(addr), "d"(v));
-}
-// predicated DSMEM store (no branch around the asm, so the chunk stays straight-line code)
-__device__ __forceinline__ void st_remote_if(bool p, uint32_t addr, double v) {
-    asm volatile(
-        "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q st.shared::cluster.f64 [%0], %1;\n\t}" ::"r"(addr),
-        "d"(v), "r"(static_cast<int>(p)));
-}
-__device__ __forceinline__ void st_remote_u32(uint32_t addr, uint32_t v) {
-    asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(addr), "r"(v));
-}
-__device__ __forceinline__ void cluster_barrier() {
-    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-__device__ __forceinline__ uint32_t cluster_rank() {
-    uint32_t r;
-    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-    return r;
-}
 
 __global__ void __launch_bounds__(kNmp, 1) cluster_kernel(ClArgs A) {
     const int cl = A.cl;
