@@ -146,6 +146,16 @@ vx_status vx_device_info(vx_ctx* ctx, int32_t* sm_count, int32_t* clock_khz, cha
  * vs glibc).  params: P x param_count, bmat: P x 3m (device pointers). */
 vx_status vx_sample_genomes_dev(vx_ctx* ctx, const vx_arch* a, int32_t P, const uint64_t* d_seeds, double* d_params,
                                 double* d_bmat);
+/* Host-pointer variant: seeds (P), params (P x param_count), bmat (P x 3m). */
+vx_status vx_sample_genomes(vx_ctx* ctx, const vx_arch* a, int32_t P, const uint64_t* seeds, double* params,
+                            double* bmat);
+/* forward (genome.hpp:187-211), the pure spatial query, for P genomes x
+ * n_points points each (host pointers): points [P][n_points][3] in the unit
+ * cube frame, probs [P][n_points][5] (max-subtracted softmax of the material
+ * head), weight [P][n_points] (stable sigmoid of the weight head, unclamped).
+ * Device tanh/exp: rtol ~1e-13 against glibc. */
+vx_status vx_forward(vx_ctx* ctx, const vx_arch* a, int32_t P, const double* params, const double* bmat,
+                     int32_t n_points, const double* points, double* probs, double* weight);
 /* decode for P genomes (morphology.hpp:141-157 over forward, genome.hpp:187-211):
  * materials (u8, argmax strict-> ties low) and clamped weights per cell,
  * cells in x-fastest order.  d_guard (optional, 1 u32) counts voxels whose top-2
@@ -333,6 +343,31 @@ vx_status vx_fp64_peak(vx_ctx* ctx, double* tflops);
 vx_status vx_fastmath_check(vx_ctx* ctx, int64_t n, uint64_t seed, int64_t* mismatches);
 
 /* ------------------------------------------------------------- bench ---- */
+/* ------------------------------------------------ Rng + GA operators (host) */
+/* Rng (rng.hpp:15-56): std::mt19937_64 with the reference's uniform01,
+ * Box-Muller normal (glibc log/cos, two fresh draws), unbiased index and
+ * libstdc++ text state.  Host only; no device needed. */
+typedef struct vx_rng vx_rng;
+vx_status vx_rng_create(uint64_t seed, vx_rng** out);
+void vx_rng_free(vx_rng* r);
+uint64_t vx_rng_next_u64(vx_rng* r);
+double vx_rng_uniform01(vx_rng* r);
+double vx_rng_normal(vx_rng* r);
+uint64_t vx_rng_index(vx_rng* r, uint64_t n);
+/* state text into buf (cap bytes incl. NUL); returns its full length */
+int64_t vx_rng_state(vx_rng* r, char* buf, int64_t cap);
+vx_status vx_rng_set_state(vx_rng* r, const char* state);
+/* crossover (evolution.hpp:143-155) on flat parameter vectors: child[i] =
+ * b[i] where uniform01 < 0.5, else a[i] (the encoding matrix stays a's: the
+ * caller copies it) */
+vx_status vx_crossover(vx_rng* r, int64_t np, const double* a, const double* b, double* child);
+/* mutate (evolution.hpp:160-165) in place: params[i] += normal*scale where
+ * uniform01 < rate, draws in parameter order */
+vx_status vx_mutate(vx_rng* r, int64_t np, double* params, double rate, double scale);
+/* tournament_select (evolution.hpp:169-173): the lowest of `size` index(P)
+ * draws — an index into the best-first sorted population */
+int32_t vx_tournament_select(vx_rng* r, int32_t population, int32_t size);
+
 /* run_bench (bench.hpp:50-86): `jobs` copies of bench_robot(grid) stepped
  * `steps` times on device.  out = springs_per_robot, spring_updates,
  * expected_updates, seconds (device time), updates_per_second, diverged. */

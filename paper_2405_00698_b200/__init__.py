@@ -275,6 +275,19 @@ def _declare(lib):
         "vx_fastmath_check": (i32, [vp, i64, u64, vp]),
         "vx_format_doubles": (i64, [vp, i64, C.c_char, C.c_char_p, i64]),
         "vx_fnv1a64": (u64, [C.c_char_p, i64]),
+        "vx_sample_genomes": (i32, [vp, P(Arch), i32, vp, vp, vp]),
+        "vx_forward": (i32, [vp, P(Arch), i32, vp, vp, i32, vp, vp, vp]),
+        "vx_rng_create": (i32, [u64, P(vp)]),
+        "vx_rng_free": (None, [vp]),
+        "vx_rng_next_u64": (u64, [vp]),
+        "vx_rng_uniform01": (dbl, [vp]),
+        "vx_rng_normal": (dbl, [vp]),
+        "vx_rng_index": (u64, [vp, u64]),
+        "vx_rng_state": (i64, [vp, C.c_char_p, i64]),
+        "vx_rng_set_state": (i32, [vp, C.c_char_p]),
+        "vx_crossover": (i32, [vp, i64, vp, vp, vp]),
+        "vx_mutate": (i32, [vp, i64, vp, dbl, dbl]),
+        "vx_tournament_select": (i32, [vp, i32, i32]),
     }
     for name, (res, args) in sigs.items():
         fn = getattr(lib, name)
@@ -411,6 +424,114 @@ def decode(genomes_params: np.ndarray, genomes_bmat: np.ndarray, arch: Arch, w: 
     wt = np.zeros((P, cells))
     _check(_lib().vx_decode(ctx.h, C.byref(arch), P, _ptr(params), _ptr(bmat), w, h, d, _ptr(mat), _ptr(wt)), "decode")
     return mat, wt
+
+
+def sample_genome(arch: Arch, seed: int, ctx: Optional[Context] = None):
+    """sample_genome(spec, hidden, seed) (genome.hpp:146-166) -> (flat params,
+    b_matrix); W bit-exact, B within ulps of glibc's normal()."""
+    p, b = sample_genomes(arch, [seed], ctx)
+    return p[0], b[0]
+
+
+def sample_genomes(arch: Arch, seeds: Sequence[int], ctx: Optional[Context] = None):
+    """sample_genome for many seeds in one launch -> (P x np params, P x 3m b_matrix)."""
+    ctx = ctx or default_context()
+    sd = np.ascontiguousarray(np.asarray(seeds, dtype=np.uint64))
+    P = len(sd)
+    params = np.zeros((P, param_count(arch)))
+    bmat = np.zeros((P, 3 * arch.m))
+    _check(_lib().vx_sample_genomes(ctx.h, C.byref(arch), P, _ptr(sd), _ptr(params), _ptr(bmat)), "sample_genome")
+    return params, bmat
+
+
+def forward(params: np.ndarray, bmat: np.ndarray, arch: Arch, points: np.ndarray, ctx: Optional[Context] = None):
+    """forward(genome, v) (genome.hpp:187-211), the pure spatial query, for
+    one genome at many points (points: n x 3) or P genomes at n points each
+    (params P x np, points P x n x 3) -> (probs [..., 5], weight [...])."""
+    ctx = ctx or default_context()
+    single = np.asarray(params).ndim == 1
+    prm = np.ascontiguousarray(np.atleast_2d(params), np.float64)
+    bm = np.ascontiguousarray(np.atleast_2d(bmat), np.float64)
+    P = prm.shape[0]
+    pts = np.ascontiguousarray(np.asarray(points, np.float64).reshape(P, -1, 3))
+    n = pts.shape[1]
+    probs = np.zeros((P, n, NMAT))
+    wt = np.zeros((P, n))
+    _check(_lib().vx_forward(ctx.h, C.byref(arch), P, _ptr(prm), _ptr(bm), n, _ptr(pts), _ptr(probs), _ptr(wt)),
+           "forward")
+    return (probs[0], wt[0]) if single else (probs, wt)
+
+
+class Rng:
+    """Rng (rng.hpp:15-56) over the library's host mt19937_64: next_u64,
+    uniform01, normal (Box-Muller, glibc), index, text state interoperable
+    with the reference's Rng::state / set_state."""
+
+    def __init__(self, seed: int = 0):
+        h = C.c_void_p()
+        _check(_lib().vx_rng_create(int(seed), C.byref(h)), "Rng")
+        self.h = h
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            _lib().vx_rng_free(self.h)
+            self.h = None
+
+    def next_u64(self) -> int:
+        return int(_lib().vx_rng_next_u64(self.h))
+
+    def uniform01(self) -> float:
+        return float(_lib().vx_rng_uniform01(self.h))
+
+    def normal(self) -> float:
+        return float(_lib().vx_rng_normal(self.h))
+
+    def index(self, n: int) -> int:
+        if n <= 0:
+            raise ValueError("Rng::index: n must be positive")
+        return int(_lib().vx_rng_index(self.h, int(n)))
+
+    def state(self) -> str:
+        n = _lib().vx_rng_state(self.h, None, 0)
+        buf = C.create_string_buffer(int(n) + 1)
+        _lib().vx_rng_state(self.h, buf, int(n) + 1)
+        return buf.value.decode()
+
+    def set_state(self, s: str):
+        _check(_lib().vx_rng_set_state(self.h, s.encode()), "Rng::set_state")
+
+    def __eq__(self, other) -> bool:
+        return isinstance(other, Rng) and self.state() == other.state()
+
+
+def crossover(a_params: np.ndarray, b_params: np.ndarray, rng: Rng, a_bmat: Optional[np.ndarray] = None,
+              b_bmat: Optional[np.ndarray] = None):
+    """crossover(a, b, rng) (evolution.hpp:143-155): uniform per-parameter mix,
+    the encoding matrix copied from a.  Returns the child's params (and its
+    b_matrix when a_bmat is given).  Parents of different architecture raise
+    ShapeMismatch."""
+    a = np.ascontiguousarray(a_params, np.float64)
+    b = np.ascontiguousarray(b_params, np.float64)
+    if a.shape != b.shape or (a_bmat is not None and b_bmat is not None and np.shape(a_bmat) != np.shape(b_bmat)):
+        raise ShapeMismatch("crossover: parents differ in architecture")
+    child = np.empty_like(a)
+    _check(_lib().vx_crossover(rng.h, a.size, _ptr(a), _ptr(b), _ptr(child)), "crossover")
+    return child if a_bmat is None else (child, np.array(a_bmat, np.float64, copy=True))
+
+
+def mutate(params: np.ndarray, rate: float, scale: float, rng: Rng) -> None:
+    """mutate(g, rate, scale, rng) (evolution.hpp:160-165), in place."""
+    if not (isinstance(params, np.ndarray) and params.dtype == np.float64 and params.flags.c_contiguous):
+        raise ValueError("mutate: params must be a contiguous float64 array (mutated in place)")
+    _check(_lib().vx_mutate(rng.h, params.size, _ptr(params), float(rate), float(scale)), "mutate")
+
+
+def tournament_select(population: int, size: int, rng: Rng) -> int:
+    """tournament_select(pop, size, rng) (evolution.hpp:169-173): index of the
+    winner in the best-first sorted population of `population` individuals."""
+    if population < 1:
+        raise ValueError("tournament_select: empty population")
+    return int(_lib().vx_tournament_select(rng.h, int(population), int(size)))
 
 
 def largest_component(mats: np.ndarray, w: int, h: int, d: int, ctx: Optional[Context] = None) -> np.ndarray:

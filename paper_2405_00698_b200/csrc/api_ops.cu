@@ -26,6 +26,46 @@ vx_status vx_sample_genomes_dev(vx_ctx* ctx, const vx_arch* a, int32_t P, const 
     return sample_genomes_dev(ctx, a, P, d_seeds, d_params, d_bmat);
 }
 
+vx_status vx_sample_genomes(vx_ctx* ctx, const vx_arch* a, int32_t P, const uint64_t* seeds, double* params,
+                            double* bmat) {
+    if (!ctx || !a || P < 0 || (P > 0 && (!seeds || !params || !bmat))) return VX_EINVAL;
+    const int64_t np = param_count(a);
+    if (np < 0) return (set_error("invalid architecture"), VX_EINVAL);
+    if (P == 0) return VX_OK;
+    DevBuf<uint64_t> ds;
+    DevBuf<double> dp, db;
+    VX_TRY(upload(ds, seeds, static_cast<size_t>(P), ctx->stream));
+    VX_TRY(dp.alloc(P * static_cast<size_t>(np)));
+    VX_TRY(db.alloc(P * 3ull * a->m));
+    VX_TRY(sample_genomes_dev(ctx, a, P, ds.p, dp.p, db.p));
+    VX_CUDA(cudaMemcpyAsync(params, dp.p, P * static_cast<size_t>(np) * sizeof(double), cudaMemcpyDeviceToHost,
+                            ctx->stream));
+    VX_CUDA(cudaMemcpyAsync(bmat, db.p, P * 3ull * a->m * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    VX_CUDA(cudaStreamSynchronize(ctx->stream));
+    return VX_OK;
+}
+
+vx_status vx_forward(vx_ctx* ctx, const vx_arch* a, int32_t P, const double* params, const double* bmat,
+                     int32_t n_points, const double* points, double* probs, double* weight) {
+    if (!ctx || !a || P < 0 || n_points < 0) return VX_EINVAL;
+    if (P == 0 || n_points == 0) return VX_OK;
+    if (!params || !bmat || !points || !probs || !weight) return VX_EINVAL;
+    const int64_t np = param_count(a);
+    if (np < 0) return (set_error("invalid architecture"), VX_EINVAL);
+    const size_t nq = static_cast<size_t>(P) * n_points;
+    DevBuf<double> dp, db, dq, dpr, dw;
+    VX_TRY(upload(dp, params, P * static_cast<size_t>(np), ctx->stream));
+    VX_TRY(upload(db, bmat, P * 3ull * a->m, ctx->stream));
+    VX_TRY(upload(dq, points, 3 * nq, ctx->stream));
+    VX_TRY(dpr.alloc(VX_NMAT * nq));
+    VX_TRY(dw.alloc(nq));
+    VX_TRY(forward_dev(ctx, a, P, dp.p, db.p, n_points, dq.p, dpr.p, dw.p));
+    VX_CUDA(cudaMemcpyAsync(probs, dpr.p, VX_NMAT * nq * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    VX_CUDA(cudaMemcpyAsync(weight, dw.p, nq * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    VX_CUDA(cudaStreamSynchronize(ctx->stream));
+    return VX_OK;
+}
+
 vx_status vx_decode_dev(vx_ctx* ctx, const vx_arch* a, int32_t P, const double* d_params, const double* d_bmat,
                         int32_t w, int32_t h, int32_t d, uint8_t* d_mat, double* d_weight, uint32_t* d_guard) {
     if (!ctx || !a || P < 0) return VX_EINVAL;

@@ -61,6 +61,12 @@ struct DecodeArgs {
     double* weight;
     uint32_t* guard;
     bool params_in_smem;
+    // forward() point queries instead of voxel centres (genome.hpp:187-211):
+    // points [genome][n_points][3]; probs [genome][n_points][5] and the
+    // unclamped weight head into `weight`
+    const double* points;
+    double* probs;
+    int n_points;
 };
 
 __device__ __forceinline__ double stable_sigmoid(double z) {
@@ -99,13 +105,18 @@ __global__ void __launch_bounds__(kThreads) decode_kernel(DecodeArgs A) {
     for (int q = threadIdx.x; q < 3 * A.m; q += kThreads) Bm[q] = A.bmat[static_cast<size_t>(g) * 3 * A.m + q];
     __syncthreads();
 
-    const int ncell = A.w * A.h * A.d;
+    const int ncell = A.points ? A.n_points : A.w * A.h * A.d;
     const int m = A.m;
     for (int t0 = 0; t0 < ncell; t0 += kTile) {
         const int cell = t0 + lane;
         const bool live = cell < ncell;
         double v0 = 0.0, v1 = 0.0, v2 = 0.0;
-        if (live) {
+        if (live && A.points) {
+            const double* pt = A.points + (static_cast<size_t>(g) * ncell + cell) * 3;
+            v0 = pt[0];
+            v1 = pt[1];
+            v2 = pt[2];
+        } else if (live) {
             const int x = cell % A.w, y = (cell / A.w) % A.h, z = cell / (A.w * A.h);
             v0 = (x + 0.5) / A.w;  // morphology.hpp:147
             v1 = (y + 0.5) / A.h;
@@ -167,20 +178,24 @@ __global__ void __launch_bounds__(kThreads) decode_kernel(DecodeArgs A) {
                 sum += p[i];
             }
             for (int i = 0; i < VX_NMAT; ++i) p[i] /= sum;
-            int best = 0;
-            for (int i = 1; i < VX_NMAT; ++i)
-                if (p[i] > p[best]) best = i;
-            if (A.guard) {
-                double second = -1.0;
-                for (int i = 0; i < VX_NMAT; ++i)
-                    if (i != best && p[i] > second) second = p[i];
-                if (p[best] - second < 1e-12 * p[best]) atomicAdd(A.guard, 1u);
-            }
-            double wgt = stable_sigmoid(L[VX_NMAT * kTile + lane]);
-            wgt = wgt < kMinVoxelWeight ? kMinVoxelWeight : (wgt > 1.0 ? 1.0 : wgt);  // morphology.hpp:154
             const size_t o = static_cast<size_t>(g) * ncell + cell;
-            A.mat[o] = static_cast<uint8_t>(best);
-            A.weight[o] = wgt;
+            const double wgt = stable_sigmoid(L[VX_NMAT * kTile + lane]);
+            if (A.probs) {  // forward(): MaterialQuery{probs, weight}
+                for (int i = 0; i < VX_NMAT; ++i) A.probs[o * VX_NMAT + i] = p[i];
+                A.weight[o] = wgt;
+            } else {  // decode(): argmax material, clamped weight
+                int best = 0;
+                for (int i = 1; i < VX_NMAT; ++i)
+                    if (p[i] > p[best]) best = i;
+                if (A.guard) {
+                    double second = -1.0;
+                    for (int i = 0; i < VX_NMAT; ++i)
+                        if (i != best && p[i] > second) second = p[i];
+                    if (p[best] - second < 1e-12 * p[best]) atomicAdd(A.guard, 1u);
+                }
+                A.mat[o] = static_cast<uint8_t>(best);
+                A.weight[o] = wgt < kMinVoxelWeight ? kMinVoxelWeight : (wgt > 1.0 ? 1.0 : wgt);  // morphology.hpp:154
+            }
         }
         __syncthreads();
     }
@@ -316,6 +331,8 @@ __global__ void __launch_bounds__(kSampleWarps * 32) sample_kernel(SampleArgs A)
 
 }  // namespace
 
+vx_status launch_decode(vx_ctx* ctx, const vx_arch* a, int64_t np, int maxw, DecodeArgs& A, int n);
+
 vx_status decode_dev(vx_ctx* ctx, const vx_arch* a, int P, const double* d_params, const double* d_bmat, int w, int h,
                      int d, uint8_t* d_mat, double* d_weight, uint32_t* d_guard, const int32_t* d_select,
                      int n_select) {
@@ -343,6 +360,34 @@ vx_status decode_dev(vx_ctx* ctx, const vx_arch* a, int P, const double* d_param
     A.mat = d_mat;
     A.weight = d_weight;
     A.guard = d_guard;
+    return launch_decode(ctx, a, np, maxw, A, n);
+}
+
+vx_status forward_dev(vx_ctx* ctx, const vx_arch* a, int P, const double* d_params, const double* d_bmat,
+                      int n_points, const double* d_points, double* d_probs, double* d_weight) {
+    const int64_t np = param_count(a);
+    if (np < 0) return (set_error("invalid architecture"), VX_EINVAL);
+    if (P <= 0 || n_points <= 0) return VX_OK;
+    DecodeArgs A{};
+    A.m = a->m;
+    A.nh = a->n_hidden;
+    int maxw = 2 * a->m;
+    for (int l = 0; l < a->n_hidden; ++l) {
+        A.widths[l] = a->hidden[l];
+        maxw = maxw > a->hidden[l] ? maxw : a->hidden[l];
+    }
+    A.np = np;
+    A.max_width = maxw;
+    A.params = d_params;
+    A.bmat = d_bmat;
+    A.points = d_points;
+    A.probs = d_probs;
+    A.n_points = n_points;
+    A.weight = d_weight;
+    return launch_decode(ctx, a, np, maxw, A, P);
+}
+
+vx_status launch_decode(vx_ctx* ctx, const vx_arch* a, int64_t np, int maxw, DecodeArgs& A, int n) {
     const size_t act = (2ull * maxw + VX_NMAT + 1) * kTile * sizeof(double) + 3ull * a->m * sizeof(double);
     size_t smem = act + static_cast<size_t>(np) * sizeof(double);
     A.params_in_smem = smem + 1024 <= ctx->smem_optin;
