@@ -105,3 +105,23 @@ def test_tournament_matches_reference_draws(vx, ref, P, size):
     idx = ref.rng_index(17, 50 * size, P)
     want = [int(min(idx[k * size:(k + 1) * size])) for k in range(50)]
     assert got == want
+
+
+def test_rng_reference_unit_cases(vx):
+    """test_rng.cpp:19-57 restated on the library's Rng."""
+    r = vx.Rng(1)
+    u = np.array([r.uniform01() for _ in range(100000)])
+    assert u.min() >= 0.0 and u.max() < 1.0 and abs(u.mean() - 0.5) < 0.01
+    r = vx.Rng(2)
+    x = np.array([r.normal() for _ in range(100000)])
+    assert np.isfinite(x).all() and abs(x.mean()) < 0.02 and abs(x.var() - 1.0) < 0.03
+    r = vx.Rng(3)
+    k = [r.index(7) for _ in range(1000)]
+    assert set(k) == set(range(7))
+    r = vx.Rng(99)
+    for _ in range(17):
+        r.next_u64()
+    snap = r.state()
+    a = [r.next_u64(), r.uniform01(), r.normal(), r.index(1000)]
+    r.set_state(snap)
+    assert [r.next_u64(), r.uniform01(), r.normal(), r.index(1000)] == a
