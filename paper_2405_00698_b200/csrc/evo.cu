@@ -190,7 +190,13 @@ void start_plan(vx_evo* e) {
     if (e->mut_uploaded) cudaEventSynchronize(e->mut_uploaded);
     e->plan_running = true;
     e->plan_failed = false;
-    e->plan_thread = std::thread([e] { parse_plan(e); });
+    const int device = e->ctx->device;
+    e->plan_thread = std::thread([e, device] {
+        // the thread's pinned allocations must land in this rank's context,
+        // not in a fresh one on device 0 (a new host thread starts there)
+        cudaSetDevice(device);
+        parse_plan(e);
+    });
 }
 
 void join_plan(vx_evo* e) {
