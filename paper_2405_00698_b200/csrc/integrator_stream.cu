@@ -463,12 +463,15 @@ struct SymLayout {
     size_t per_robot, k, r0, vox, x0, x1, mc, mask, cph, sph, sa, amap;
 };
 
+// constexpr: the kernel folds every array of the per-robot scratch into one
+// base register plus immediate offsets (ten 64-bit pointers would cost 20 of
+// its 64 registers)
 template <int N>
-SymLayout sym_layout() {
+__host__ __device__ constexpr SymLayout sym_layout() {
     using G = SymGeom<N>;
     SymLayout L{};
     size_t o = 0;
-    auto take = [&](size_t bytes) {
+    auto take = [&o](size_t bytes) {
         const size_t at = o;
         o += (bytes + 255) / 256 * 256;
         return at;
@@ -649,7 +652,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_sym_kernel(SymArgs A
     constexpr int NV = G::NV;
     const int r = blockIdx.x;
     const BatchView& b = A.b;
-    const SymLayout& L = A.L;
+    constexpr SymLayout L = sym_layout<N>();
     const int t = threadIdx.x;
     unsigned char* base = A.scratch + static_cast<size_t>(r) * L.per_robot;
     const int NT = at<int32_t>(base, L.amap)[G::NCELL + 1];  // this robot's actuator rows + sentinel
