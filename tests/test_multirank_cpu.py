@@ -1,12 +1,15 @@
 """Multi-rank protocol on CPU (gloo, world_size 2).
 
-The GPU path shards a generation's children across ranks (vx_evo_begin), then
-all-reduces (SUM) a 2P exchange buffer holding each rank's fitness and work
-counts (zeros elsewhere) and breeds identically everywhere (vx_evo_finish).
-Here the same protocol runs with the oracle as the per-rank evaluator: the
-reduced vector must equal a single-process evaluation bit for bit, and the
-replicated breeding must give identical populations and RNG states on every
-rank — the GPU analogue of the reference's thread-count invariance
+The GPU path shards a generation's children across ranks (vx_evo_begin): a
+rank decodes and evaluates only the individuals it owns, then all-reduces
+(SUM) the (2P + 5 cells)-double exchange buffer [fitness P | work counts P |
+material histogram cells x 5] — zeros for what other ranks own — and breeds
+identically everywhere (vx_evo_finish).  Here the same protocol runs with
+the oracle as the per-rank evaluator: the reduced fitness must equal a
+single-process evaluation bit for bit, the reduced histogram must give the
+reference's population_diversity over all grids (evolution.hpp:89-105), and
+the replicated breeding must give identical populations and RNG states on
+every rank — the GPU analogue of the reference's thread-count invariance
 (test_evolution.cpp:196-215).
 """
 import os
@@ -20,7 +23,18 @@ import torch.multiprocessing as mp
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 P, GRID = 8, 3
+CELLS = GRID ** 3
 SIM = None
+
+
+def diversity_from_histogram(hist, P):
+    """diversity_kernel (csrc/ga.cu): exact integer pair counts per cell."""
+    h = np.asarray(hist, np.int64).reshape(-1, 5)
+    pairs = P * (P - 1) // 2
+    same = (h * (h - (h > 0)) // 2).sum()
+    if P < 2 or len(h) == 0:
+        return 0.0
+    return (float(pairs * len(h) - same) / len(h)) / pairs
 
 
 def _worker(rank, world, port, out_dir):
@@ -44,15 +58,21 @@ def _worker(rank, world, port, out_dir):
             m, w = lib.decode(8, [12, 12], pop["params"][a], pop["bmat"][a], GRID, GRID, GRID)
             mats.append(m)
             wts.append(w)
-        xbuf = torch.zeros(2 * P, dtype=torch.float64)
+        xbuf = torch.zeros(2 * P + 5 * CELLS, dtype=torch.float64)
         for a in vx.shard_indices(todo, rank, world):
             xbuf[a] = lib.evaluate_fitness(mats[a], wts[a], GRID, GRID, GRID, sim=sim)
             xbuf[P + a] = 1.0
+        for a in vx.shard_indices(list(range(P)), rank, world):  # the grids this rank holds
+            for c in range(CELLS):
+                xbuf[2 * P + 5 * c + int(mats[a][c])] += 1.0
         dist.all_reduce(xbuf)
         fit = pop["fitness"].copy()
         for a in todo:
             fit[a] = xbuf[a].item()
-        assert xbuf[P:].sum().item() == len(todo)  # every child evaluated exactly once
+        assert xbuf[P:2 * P].sum().item() == len(todo)  # every child evaluated exactly once
+        assert xbuf[2 * P:].sum().item() == P * CELLS     # every grid counted exactly once
+        div = diversity_from_histogram(xbuf[2 * P:].numpy().astype(np.int64), P)
+        np.testing.assert_allclose(div, lib.population_diversity(np.stack(mats)), rtol=1e-13)
         ev.set_population(pop["params"], pop["bmat"], fit, np.ones(P, np.uint8), np.stack(mats), np.stack(wts))
         rep = ev.generation()
         np.save(os.path.join(out_dir, f"r{rank}_g{gen}_fit.npy"), fit)
