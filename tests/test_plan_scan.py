@@ -8,6 +8,7 @@ import json
 import os
 import subprocess
 
+import numpy as np
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -38,3 +39,18 @@ def test_plan_scan_matches_restated_loop(plan_check, P, np_, cx, rate, gens, ski
     assert out.returncode == 0, out.stdout + out.stderr
     r = json.loads(out.stdout.strip().splitlines()[-1])
     assert r["ok"] is True
+
+
+def test_plan_scan_random_sweep(plan_check):
+    """Random shapes and rates (a fixed-seed sweep): every combination must
+    reproduce the restated loop bit for bit."""
+    rng = np.random.default_rng(2405)
+    for _ in range(12):
+        P = int(rng.integers(2, 400))
+        np_ = int(rng.integers(1, 5000))
+        cx = float(rng.choice([0.0, 1.0, rng.random()]))
+        rate = float(rng.choice([0.0, 1.0, rng.random() * 0.3, rng.random()]))
+        skip = int(rng.integers(0, 700))
+        out = subprocess.run([plan_check, str(P), str(np_), repr(cx), repr(rate), "2", str(skip)],
+                             capture_output=True, text=True, timeout=120)
+        assert out.returncode == 0, (P, np_, cx, rate, skip, out.stdout)
