@@ -146,6 +146,10 @@ vx_status vx_device_info(vx_ctx* ctx, int32_t* sm_count, int32_t* clock_khz, cha
  * vs glibc).  params: P x param_count, bmat: P x 3m (device pointers). */
 vx_status vx_sample_genomes_dev(vx_ctx* ctx, const vx_arch* a, int32_t P, const uint64_t* d_seeds, double* d_params,
                                 double* d_bmat);
+/* gaussian_encode (genome.hpp:168-179) of one point v[3] with the m x 3
+ * encoding matrix: out[r] = cos(2 pi B_r . v), out[m + r] = sin(...); host
+ * libm, bit-identical to the reference on the same machine. */
+vx_status vx_gaussian_encode(const double* v, const double* bmat, int32_t m, double* out);
 /* Host-pointer variant: seeds (P), params (P x param_count), bmat (P x 3m). */
 vx_status vx_sample_genomes(vx_ctx* ctx, const vx_arch* a, int32_t P, const uint64_t* seeds, double* params,
                             double* bmat);

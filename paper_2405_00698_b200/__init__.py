@@ -276,6 +276,7 @@ def _declare(lib):
         "vx_format_doubles": (i64, [vp, i64, C.c_char, C.c_char_p, i64]),
         "vx_fnv1a64": (u64, [C.c_char_p, i64]),
         "vx_sample_genomes": (i32, [vp, P(Arch), i32, vp, vp, vp]),
+        "vx_gaussian_encode": (i32, [vp, vp, i32, vp]),
         "vx_forward": (i32, [vp, P(Arch), i32, vp, vp, i32, vp, vp, vp]),
         "vx_rng_create": (i32, [u64, P(vp)]),
         "vx_rng_free": (None, [vp]),
@@ -424,6 +425,18 @@ def decode(genomes_params: np.ndarray, genomes_bmat: np.ndarray, arch: Arch, w: 
     wt = np.zeros((P, cells))
     _check(_lib().vx_decode(ctx.h, C.byref(arch), P, _ptr(params), _ptr(bmat), w, h, d, _ptr(mat), _ptr(wt)), "decode")
     return mat, wt
+
+
+def gaussian_encode(v, bmat: np.ndarray, m: int) -> np.ndarray:
+    """gaussian_encode(v, B, m) (genome.hpp:168-179) -> the 2m Fourier
+    features of one point (host libm: bit-identical to the reference)."""
+    vv = np.ascontiguousarray(v, np.float64).reshape(3)
+    b = np.ascontiguousarray(bmat, np.float64).reshape(-1)
+    if b.size != 3 * m:
+        raise ShapeMismatch("gaussian_encode: encoding matrix size does not match m")
+    out = np.zeros(2 * m)
+    _check(_lib().vx_gaussian_encode(_ptr(vv), _ptr(b), int(m), _ptr(out)), "gaussian_encode")
+    return out
 
 
 def sample_genome(arch: Arch, seed: int, ctx: Optional[Context] = None):

@@ -125,3 +125,14 @@ def test_rng_reference_unit_cases(vx):
     a = [r.next_u64(), r.uniform01(), r.normal(), r.index(1000)]
     r.set_state(snap)
     assert [r.next_u64(), r.uniform01(), r.normal(), r.index(1000)] == a
+
+
+def test_gaussian_encode_matches_reference(vx, ref):
+    """gaussian_encode (genome.hpp:168-179), host ABI, bit for bit."""
+    rng = np.random.default_rng(8)
+    for m in (1, 4, 32):
+        b = rng.normal(size=3 * m)
+        for v in (rng.random(3), rng.normal(0, 5, 3), np.zeros(3)):
+            np.testing.assert_array_equal(vx.gaussian_encode(v, b, m), ref.gaussian_encode(v, b, m))
+    with pytest.raises(vx.ShapeMismatch):
+        vx.gaussian_encode(np.zeros(3), np.zeros(5), 2)
