@@ -133,6 +133,29 @@ inline Genome unflatten(const EvolutionConfig& cfg, const double* params, const 
     return g;
 }
 
+// forward (genome.hpp:187-211) for a batch of query points of one genome
+// (one launch); MaterialQuery per point.
+inline std::vector<MaterialQuery> forward(const Genome& g, const std::vector<Vec3>& points,
+                                          Device& dev = default_device()) {
+    std::vector<MaterialQuery> out(points.size());
+    if (points.empty()) return out;
+    const vx_arch a = to_c(g);
+    std::vector<double> params, pts(3 * points.size()), probs(5 * points.size()), wt(points.size());
+    flatten(g, params);
+    for (size_t q = 0; q < points.size(); ++q)
+        for (int c = 0; c < 3; ++c) pts[3 * q + c] = points[q][c];
+    check(vx_forward(dev.get(), &a, 1, params.data(), g.b_matrix.data(), static_cast<int32_t>(points.size()),
+                     pts.data(), probs.data(), wt.data()));
+    for (size_t q = 0; q < points.size(); ++q) {
+        for (int i = 0; i < 5; ++i) out[q].probs[i] = probs[5 * q + i];
+        out[q].weight = wt[q];
+    }
+    return out;
+}
+inline MaterialQuery forward(const Genome& g, const Vec3& v, Device& dev = default_device()) {
+    return forward(g, std::vector<Vec3>{v}, dev)[0];
+}
+
 // decode (morphology.hpp:141-157)
 inline VoxelGrid decode(const Genome& g, int w, int h, int d, Device& dev = default_device()) {
     if (w < 1 || h < 1 || d < 1) throw std::invalid_argument("decode: dims must be positive");

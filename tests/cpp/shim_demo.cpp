@@ -76,6 +76,21 @@ int main() {
     report("simulate with dump every 300 steps: rows and times match", dump_ok,
            std::to_string(rd.size()) + " rows");
 
+    // forward (genome.hpp:187-211) at off-grid points: probabilities and weight within 1e-12
+    {
+        const Genome fg = sample_genome(EncodingSpec{32, 3, 1.0}, {64, 64}, 77);
+        const std::vector<Vec3> pts = {{0.1, 0.2, 0.3}, {0.9, 0.05, 0.5}, {-2.0, 3.5, 0.25}};
+        const std::vector<MaterialQuery> gq = b200::forward(fg, pts);
+        bool fok = true;
+        for (size_t q = 0; q < pts.size(); ++q) {
+            const MaterialQuery rq = forward(fg, pts[q]);
+            for (int i = 0; i < 5; ++i) fok = fok && std::abs(rq.probs[i] - gq[q].probs[i]) <= 1e-12 * rq.probs[i] + 1e-300;
+            fok = fok && std::abs(rq.weight - gq[q].weight) <= 1e-12 * rq.weight;
+        }
+        report("forward at off-grid points: probs / weight <= 1e-12", fok, std::to_string(pts.size()) + " points");
+    }
+
+
     // desk GA (acceptance_main.cpp:193-211 shape): reference genomes on the
     // GPU; draw consumption is fitness-independent -> identical RNG streams
     EvolutionConfig cfg;
