@@ -1,31 +1,42 @@
 #!/usr/bin/env python
 """bench.py — spring-mass updates/s of the voxevo hot path on B200.
 
-(--workload config3 / config5 run BASELINE configs 3 / 5 under the same
-contract: one generation of P=4096 10^3 / P=1024 20^3 robots per step.)
+Workload (default, BASELINE.json configs[2], "config 3" — the largest
+single-GPU configuration): population 4096 of 10x10x10 voxel robots per GPU,
+evolve_generation (evolution.hpp:217-293) with elite selection / crossover /
+mutation at the reference defaults, 5000-step fitness (dt 1e-5).  A bench
+STEP is ONE generation of ONE continuing run: generation 0 (all P robots
+decoded and evaluated) is the first warm-up step, every later step is the next
+generation (~0.7P children decoded, assembled, simulated; elites keep their
+cached fitness, exactly like the reference).  Work differs slightly between
+generations, so
 
-Workload (BASELINE.json configs[1], "config 2"): population 256 of 6x6x6 voxel
-robots per GPU, ONE generation = decode (Fourier encoding + MLP) -> largest
-component -> mass-spring assembly -> 5000-step fused integrator (dt 1e-5) ->
-fitness -> stable sort / stats / diversity -> elite + tournament / crossover /
-mutation breeding.  A bench "step" is one such generation from the same
-synthetic generation-0 population (genomes sampled on device from seed 42 with
-the reference's mt19937_64 streams), so every step does identical work.
+  value : sum of the EXACT spring updates of the K timed generations / sum of
+          their device time (CUDA events on the context stream), population
+          resident in HBM
+  e2e   : K further generations of the same run through the public API with
+          the population HOST-resident in pinned memory: every step uploads
+          the population (genomes, fitness, evaluated flags) and downloads the
+          bred population plus fitness, both inside the timed region
+  generations_per_s : K / sum of the device time
 
-  value : whole-job spring updates/s with the genomes already resident in HBM
-  e2e   : the same through the public API with the genomes copied host(pinned)
-          -> device and the fitness vector copied back inside the timed region
-Multi-GPU (torchrun): weak scaling, 256 robots evaluated per GPU; the
-population (256*N) is replicated, children are sharded, one NCCL all-reduce
-of the fitness exchange buffer per generation.
+--workload config2 / config5 run P=256 6^3 / P=1024 20^3 the same way.
+Multi-GPU (torchrun, or --gpus N which relaunches itself under torchrun):
+weak scaling, P = 4096 per GPU; the population is replicated, the children
+are sharded, and the library's own NCCL communicator (vx_comm_create)
+all-reduces the exchange buffer once per generation.
 
 --impl reference runs the reference's own CPU implementation (the compiled,
-unmodified reference headers in oracle/_ref) through evolve_generation with
-all host threads on the same config.
+unmodified reference headers in oracle/_ref): successive evolve_generation
+calls of a bounded population (P=64 of the same grid; 256 for config 2) with
+every host thread, each step timed alone and audited for its exact spring
+updates outside the timed region.
 """
 import argparse
 import json
 import os
+import platform
+import socket
 import subprocess
 import sys
 import threading
@@ -36,32 +47,57 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-P_PER_GPU = 256
-GRID = 6
 SIM_STEPS = 5000
-# --workload: the default is config 2 (BASELINE.json configs[1], the driver's
-# line); configs 3 and 5 run one generation of their population per step
-WORKLOADS = {
-    "config2": dict(P=256, grid=6, kernel="vertex_kernel<6> (fused integrator K7-K9, vertex-key-indexed)",
-                    desc="config 2: P=256 6x6x6 per GPU, 1 generation (decode + 5000-step fitness + sort/stats/"
-                         "diversity + breed)"),
-    "config3": dict(P=4096, grid=10, kernel="cluster_vertex_kernel<10> (4-CTA thread-block cluster per robot)",
-                    desc="config 3: P=4096 10x10x10 per GPU, 1 of the 50 generations per step (decode + "
-                         "5000-step fitness + sort/stats/diversity + breed)"),
-    "config5": dict(P=1024, grid=20, kernel="stream_sym_kernel<20> (symmetric streaming integrator)",
-                    desc="config 5: P=1024 20x20x20 per GPU, 1 generation (decode + 5000-step fitness + sort/"
-                         "stats/diversity + breed)"),
-}
-CPU_SAMPLE_MAX = 256  # robots in the bounded cpu_baseline sample
 DT = 1e-5
 SEED = 42
 FLOPS_PER_UPDATE = 48  # 48 FP64 flop (+1 sqrt +1 div) per spring update
 METRIC = "spring-mass updates/sec (1/2/4/8 B200) and generations/sec at fixed population"
+WORKLOADS = {
+    "config3": dict(P=4096, grid=10, ref_P=64, cpu_sample=32,
+                    kernel="cluster_vertex_kernel<10> (4-CTA thread-block cluster per robot)",
+                    traffic="cluster_traffic.json",
+                    desc="config 3: population 4096 of 10x10x10 robots per GPU, successive generations of one run "
+                         "(elite selection / crossover / mutation, 5000-step fitness)"),
+    "config2": dict(P=256, grid=6, ref_P=256, cpu_sample=256,
+                    kernel="vertex_kernel<6> (fused integrator K7-K9, vertex-key-indexed)",
+                    traffic="integrator_traffic.json",
+                    desc="config 2: population 256 of 6x6x6 robots per GPU, successive generations of one run "
+                         "(decode + 5000-step fitness + sort/stats/diversity + breed)"),
+    "config5": dict(P=1024, grid=20, ref_P=8, cpu_sample=8,
+                    kernel="stream_sym_kernel<20> (symmetric streaming integrator)",
+                    traffic="stream_traffic.json",
+                    desc="config 5: population 1024 of 20x20x20 robots per GPU, successive generations of one run "
+                         "(5000-step fitness, streaming integrator)"),
+}
 
 
 def rank_info():
     return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), int(
         os.environ.get("LOCAL_RANK", "0"))
+
+
+def host_info() -> dict:
+    """CPU model, glibc and the libm variant glibc's ifunc picks."""
+    model = platform.processor() or "unknown"
+    flags = ""
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+            if ln.startswith("flags"):
+                flags = ln.split(":", 1)[1]
+            if model != "unknown" and flags:
+                break
+    except OSError:
+        pass
+    fl = set(flags.split())
+    libm = ("glibc ifunc FMA/AVX2 variants (__exp_fma, __sin_fma, ...)" if {"fma", "avx2"} <= fl
+            else "glibc ifunc generic (SSE2) variants")
+    try:
+        glibc = os.confstr("CS_GNU_LIBC_VERSION")
+    except (ValueError, OSError):
+        glibc = "unknown"
+    return {"cpu_model": model, "glibc": glibc, "libm_variant": libm, "host_threads": os.cpu_count() or 1}
 
 
 class ClockSampler:
@@ -79,7 +115,7 @@ class ClockSampler:
                  "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
                  "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
                  "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
-                 "--format=csv,noheader,nounits", "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                 "--format=csv,noheader,nounits", "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
                 text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -120,43 +156,21 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def flush_l2(torch, buf):
-    buf.zero_()  # 256 MiB > 126 MB L2
+def config_block(W, world):
+    """Identical in both arms (same_config)."""
+    return {"workload": W["desc"], "population_per_gpu": W["P"], "population": W["P"] * world,
+            "grid": [W["grid"]] * 3, "sim_steps": SIM_STEPS, "dt": DT, "seed": SEED,
+            "hyper": "reference defaults: elite 0.3, crossover 0.4, mutation rate 0.1 scale 0.1, tournament 3",
+            "l2": "flushed (256 MiB write) between steps", "parallelism": f"population shards x{world}"}
 
 
-def make_config(vx, P):
-    return vx.EvolutionConfig(population=P, generations=0, grid=(GRID, GRID, GRID), seed=SEED,
+def make_config(vx, P, grid):
+    return vx.EvolutionConfig(population=P, generations=0, grid=(grid, grid, grid), seed=SEED,
                               sim=vx.SimConfig(dt=DT, duration=SIM_STEPS * DT))
 
 
-def cpu_baseline_sample(grids, weights):
-    """Reference evaluate_fitness over the generation's 256 raw grids through
-    its own parallel_for with all host threads (oracle/_ref)."""
-    import oracle
-    lib = oracle.reference() if oracle.have_reference() else None
-    kind = "reference"
-    threads = os.cpu_count() or 1
-    n = grids.shape[0]
-    fit = np.zeros(n)
-    upd = np.zeros(1, np.uint64)
-    sim = oracle.sim6(dt=DT, duration=SIM_STEPS * DT)
-    if lib is None:  # restatement (single-threaded port)
-        lib = oracle.restatement()
-        kind, threads = "port", 1
-        t0 = time.perf_counter()
-        for a in range(n):
-            fit[a] = lib.evaluate_fitness(grids[a], weights[a], GRID, GRID, GRID, sim=sim)
-        secs = time.perf_counter() - t0
-        return None, dict(kind=kind, cores=1, secs=secs)
-    g = np.ascontiguousarray(grids, np.uint8)
-    w = np.ascontiguousarray(weights, np.float64)
-    secs = lib._evaluate_batch(n, GRID, GRID, GRID, g.ctypes.data, w.ctypes.data, oracle.DEFAULT_TABLE.ctypes.data,
-                               oracle.DEFAULT_PLANE.ctypes.data, sim.ctypes.data, threads, fit.ctypes.data,
-                               upd.ctypes.data)
-    return int(upd[0]), dict(kind=kind, cores=threads, secs=secs, fitness=fit)
-
-
-def run_reference(args):
+# ---------------------------------------------------------------- reference arm
+def run_reference(args, W):
     """--impl reference: the reference's evolve_generation on the host cores."""
     rank, world, _ = rank_info()
     if rank != 0:
@@ -168,57 +182,103 @@ def run_reference(args):
     ref = oracle.reference()
     threads = os.cpu_count() or 1
     sim = oracle.sim6(dt=DT, duration=SIM_STEPS * DT)
-    P = P_PER_GPU
-    ev = ref.evo(population=P, generations=0, grid=(GRID, GRID, GRID), seed=SEED, threads=threads, sim=sim)
-    pop0 = ev.population()
-    # exact work audit of one generation (outside the timed region)
-    mats = np.zeros((P, GRID ** 3), np.uint8)
-    wts = np.zeros((P, GRID ** 3))
-    for a in range(P):
-        mats[a], wts[a] = ref.decode(32, [64, 64], pop0["params"][a], pop0["bmat"][a], GRID, GRID, GRID)
-    upd, _ = cpu_baseline_sample(mats, wts)
-    times = []
+    P, g = W["ref_P"], W["grid"]
+    ev = ref.evo(population=P, generations=0, grid=(g, g, g), seed=SEED, threads=threads, sim=sim)
+    secs, upds = [], []
     for it in range(args.warmup + args.steps):
-        ev.set_population(pop0["params"], pop0["bmat"])  # generation-0 state, nothing cached
-        ev.set_rng_state(oracle.reference().rng_state(SEED, P))
-        t0 = time.perf_counter()
-        ev.generation()
-        dt_s = time.perf_counter() - t0
+        _, s, u = ev.generation_timed()
         if it >= args.warmup:
-            times.append(dt_s)
-    total = float(np.sum(times))
-    value = upd * len(times) / total
+            secs.append(s)
+            upds.append(u)
+    total = float(np.sum(secs))
+    value = float(np.sum(upds)) / total
+    sample = (f"reference evolve_generation (evolution.hpp:217-293) on a bounded population P={P} of {g}^3 robots "
+              f"(the config's grid, hyper-parameters and 5000-step fitness), successive generations "
+              f"{args.warmup}..{args.warmup + args.steps - 1} of one run, one per step, timed alone; exact spring "
+              f"updates audited outside the timed region; headers compiled -O2 no -march, std::thread parallel_for "
+              f"with {threads} threads")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "spring_updates/s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / len(times),
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / len(secs),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": args.desc, "population": P, "grid": [GRID] * 3, "sim_steps": SIM_STEPS, "dt": DT,
-                   "seed": SEED},
-        "generations_per_s": len(times) / total,
+        "config": config_block(W, world),
+        "generations_per_s": len(secs) / total,
+        "spring_updates_per_step": float(np.mean(upds)),
         "cpu_baseline": {"value": value, "unit": "spring_updates/s", "cores": threads, "kind": "reference",
-                         "sample": f"full evolve_generation (P={P}, {GRID}^3, {SIM_STEPS} steps), reference "
-                                   "headers compiled -O2 no -march, std::thread parallel_for"},
+                         "sample": sample, **host_info()},
         "e2e": {"value": value, "unit": "spring_updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
 
 
+def cpu_baseline_and_parity(W, params0, bmat0, fit0_gpu):
+    """The reference (oracle/_ref) on a bounded sample of this run's generation-0
+    robots: its own decode, then evaluate_fitness through its parallel_for on
+    every host thread (timed), and the per-robot fitness parity of the GPU
+    generation 0 against it."""
+    import oracle
+    g = W["grid"]
+    n = min(W["cpu_sample"], params0.shape[0])
+    if not oracle.have_reference():
+        return None, None
+    lib = oracle.reference()
+    threads = os.cpu_count() or 1
+    cells = g ** 3
+    mats = np.zeros((n, cells), np.uint8)
+    wts = np.zeros((n, cells))
+    for a in range(n):
+        mats[a], wts[a] = lib.decode(32, [64, 64], params0[a], bmat0[a], g, g, g)
+    fit = np.zeros(n)
+    upd = np.zeros(1, np.uint64)
+    sim = oracle.sim6(dt=DT, duration=SIM_STEPS * DT)
+    secs = lib._evaluate_batch(n, g, g, g, mats.ctypes.data, wts.ctypes.data, oracle.DEFAULT_TABLE.ctypes.data,
+                               oracle.DEFAULT_PLANE.ctypes.data, sim.ctypes.data, threads, fit.ctypes.data,
+                               upd.ctypes.data)
+    cpu = {"value": float(upd[0]) / secs, "unit": "spring_updates/s", "cores": threads, "kind": "reference",
+           "sample": f"reference decode + evaluate_fitness (evolution.hpp:110-119) of generation 0's first {n} "
+                     f"{g}^3 robots x {SIM_STEPS} steps ({int(upd[0])} updates) via its parallel_for, {secs:.2f} s",
+           **host_info()}
+    gpu = fit0_gpu[:n]
+    rel = np.abs(gpu - fit) / np.maximum(np.abs(fit), 1e-12)
+    parity = {"n": int(n), "max_rel": float(rel.max()), "median_rel": float(np.median(rel)),
+              "exact": int(np.sum(gpu == fit)), "tolerance": "max <= 1e-3, median <= 1e-4 (SURVEY.md §8(d))",
+              "ok": bool(rel.max() <= 1e-3 and np.median(rel) <= 1e-4),
+              "what": "GPU generation-0 fitness vs the reference's decode + evaluate_fitness of the same genomes"}
+    return cpu, parity
+
+
+def relaunch_under_torchrun(args):
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    sys.exit(subprocess.call(cmd))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer e2e leg (profiling runs)")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no baselines, no clocks)")
-    ap.add_argument("--workload", default="config2", choices=sorted(WORKLOADS))
+    ap.add_argument("--workload", default="config3", choices=sorted(WORKLOADS))
     args = ap.parse_args()
-    global P_PER_GPU, GRID
     W = WORKLOADS[args.workload]
-    P_PER_GPU, GRID = W["P"], W["grid"]
-    args.kernel, args.desc = W["kernel"], W["desc"]
+    rank, world, local = rank_info()
+    launched = "RANK" in os.environ and "MASTER_ADDR" in os.environ
+    if args.gpus > 1 and not launched:
+        relaunch_under_torchrun(args)
+    if launched and world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+    if args.warmup < 1:
+        raise SystemExit("bench.py: --warmup must be >= 1 (generation 0 is a warm-up step)")
     if args.impl == "reference":
-        run_reference(args)
+        run_reference(args, W)
         return
 
     import torch
@@ -226,173 +286,171 @@ def main():
 
     import paper_2405_00698_b200 as vx
 
-    rank, world, local = rank_info()
-    distributed = "RANK" in os.environ and "MASTER_ADDR" in os.environ  # launched by torchrun (any N)
     torch.cuda.set_device(local)
-    if distributed:
+    if launched:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     ctx = vx.Context(local)
     stream = torch.cuda.current_stream()
     ctx.set_stream(stream.cuda_stream)
-    P = P_PER_GPU * world
-    st = vx.init_evolution(make_config(vx, P), ctx)
-    np_ = st.np
-    nb = 3 * st.config.arch.m
-    pop0 = st.population()  # generation-0 genomes sampled on device (K14)
-    init_params = torch.from_numpy(pop0["params"]).cuda()
-    init_bmat = torch.from_numpy(pop0["bmat"]).cuda()
-    del pop0
+    P = W["P"] * world
+    st = vx.init_evolution(make_config(vx, P, W["grid"]), ctx)
+    np_, nb = st.np, 3 * st.config.arch.m
+    comm = None
+    if launched and world > 1:  # the library's own NCCL communicator does the exchange
+        obj = [vx.Communicator.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        comm = vx.Communicator(ctx, world, rank, obj[0])
+        st.set_comm(comm)
     xbuf = torch.zeros(st.exchange_buffer()[1], dtype=torch.float64, device="cuda")  # fitness|updates|histogram
     st.set_exchange_buffer(xbuf.data_ptr())
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
-    host_params = torch.empty((P, np_), dtype=torch.float64, pin_memory=True)
-    host_bmat = torch.empty((P, nb), dtype=torch.float64, pin_memory=True)
-    host_params.copy_(init_params)
-    host_bmat.copy_(init_bmat)
-    host_fit = torch.empty(P, dtype=torch.float64, pin_memory=True)
 
-    def generation(e2e: bool):
-        if e2e:
-            init_params.copy_(host_params, non_blocking=True)
-            init_bmat.copy_(host_bmat, non_blocking=True)
-        st.load_population_dev(init_params.data_ptr(), init_bmat.data_ptr())
-        st.set_rng_state(_seed_state)
-        st.begin(rank, world)
-        if distributed:
-            dist.all_reduce(xbuf)
-        rep = st.finish()
-        if e2e:
-            host_fit.copy_(xbuf[:P], non_blocking=False)
-        return rep
+    def barrier():
+        torch.cuda.synchronize()
+        if launched:
+            dist.barrier()
 
-    # RNG stream position of init_evolution's output (breeding replays identically each step)
-    _seed_state = st.rng_state()
+    # ---- warm-up: generation 0 (all P robots) and W-1 more
+    pop0 = st.population()
+    params0, bmat0 = pop0["params"], pop0["bmat"]
+    del pop0
+    fit0 = None
+    for it in range(args.warmup):
+        st.evolve_generation()
+        if it == 0:
+            fit0 = xbuf[:P].cpu().numpy().copy()  # generation-0 fitness in individual order
+    barrier()
 
-    def timed(n, e2e):
-        ms, reps = [], []
-        for _ in range(n):
-            flush_l2(torch, flush)
-            torch.cuda.synchronize()
-            if distributed:
-                dist.barrier()
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            reps.append(generation(e2e))
-            e1.record(stream)
-            torch.cuda.synchronize()
-            ms.append(e0.elapsed_time(e1))
-        return ms, reps
-
-    for _ in range(args.warmup):
-        generation(False)
-    torch.cuda.synchronize()
+    # ---- value: K generations, population resident in HBM
     ctx.timing(True)
     ctx.integrator_time(reset=True)
     launches0 = ctx.launches
+    ms, upd = [], []
     with ClockSampler(local) as clk:
-        ms, reps = timed(args.steps, e2e=False)
+        for _ in range(args.steps):
+            flush.zero_()
+            barrier()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            rep = st.evolve_generation()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ms.append(e0.elapsed_time(e1))
+            upd.append(int(rep.spring_updates))
     launches = ctx.launches - launches0
     int_ms, int_n = ctx.integrator_time(reset=True)
     ctx.timing(False)
-    ms_e2e, reps_e2e = timed(args.steps, e2e=True)
+
+    # ---- e2e: K more generations with the population host-resident (pinned)
+    ms_e2e, upd_e2e = [], []
+    h2d = d2h = 0
+    if not args.no_e2e and not args.profile:
+        hp = torch.empty((P, np_), dtype=torch.float64, pin_memory=True)
+        hb = torch.empty((P, nb), dtype=torch.float64, pin_memory=True)
+        hf = torch.empty(P, dtype=torch.float64, pin_memory=True)
+        he = torch.empty(P, dtype=torch.uint8, pin_memory=True)
+        hpn, hbn, hfn, hen = hp.numpy(), hb.numpy(), hf.numpy(), he.numpy()
+        st.get_population_into(hpn, hbn, hfn, hen)  # the run's state moves to the host
+        for _ in range(args.steps):
+            flush.zero_()
+            barrier()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            st.set_population(hpn, hbn, hfn, hen)  # H2D: genomes, fitness, evaluated flags
+            rep = st.evolve_generation()
+            st.get_population_into(hpn, hbn, hfn, hen)  # D2H: the bred population and its fitness
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ms_e2e.append(e0.elapsed_time(e1))
+            upd_e2e.append(int(rep.spring_updates))
+        h2d = d2h = P * (np_ + nb) * 8 + P * 8 + P
 
     total_ms = float(np.sum(ms))
-    total_e2e = float(np.sum(ms_e2e))
-    if distributed:
+    total_e2e = float(np.sum(ms_e2e)) if ms_e2e else 0.0
+    if launched:
         t = torch.tensor([total_ms, total_e2e], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms, total_e2e = float(t[0]), float(t[1])
-    upd_per_step = int(reps[0].spring_updates)  # whole job (exchange buffer is all-reduced)
-    assert all(int(r.spring_updates) == upd_per_step for r in reps + reps_e2e), "work differs between steps"
-    value = upd_per_step * args.steps / (total_ms * 1e-3)
-    value_e2e = upd_per_step * args.steps / (total_e2e * 1e-3)
+    value = float(np.sum(upd)) / (total_ms * 1e-3)
+    value_e2e = float(np.sum(upd_e2e)) / (total_e2e * 1e-3) if ms_e2e else None
     if rank != 0:
+        if comm is not None:
+            st.set_comm(None)
+            comm.close()
         dist.destroy_process_group()
         return
 
-    # roofline of the dominant kernel (the fused integrator), from live CUDA events
-    local_upd = upd_per_step // world
+    # roofline of the dominant kernel, from live CUDA events on the launching stream
+    local_upd = float(np.sum(upd)) / world  # this rank's share (children are dealt round-robin)
     avg_int_ms = int_ms / max(1, int_n)
-    achieved_tf = FLOPS_PER_UPDATE * local_upd / (avg_int_ms * 1e-3) / 1e12 if int_n else None
-    peak_tf = ctx.fp64_peak_tflops()
-    # the dominant kernel's roofline: FP64-issue bound on chip (configs 2, 3),
-    # HBM bound for the streaming integrator (config 5)
-    prof = {"config2": "integrator_traffic.json", "config3": "cluster_traffic.json",
-            "config5": "stream_traffic.json"}[args.workload]
-    meta = _ncu_json(prof)
-    launch_upd = local_upd
-    traffic = None
-    if meta.get("dram_bytes_per_launch") is not None and args.workload == "config2":
-        traffic = meta["dram_bytes_per_launch"]  # captured at the config-2 launch shape (batch load dominated)
-    elif meta.get("dram_bytes_per_update") is not None:
-        traffic = meta["dram_bytes_per_update"] * launch_upd
+    upd_per_launch = local_upd / max(1, int_n)
+    meta = _ncu_json(W["traffic"])
+    traffic = meta.get("dram_bytes_per_launch") if meta.get("workload") == args.workload else None
     if args.workload == "config5":
         peak_gbs, peak_src = _hbm_peak()
         ab = meta.get("algorithmic_bytes_per_update", 60)
-        achieved_gbs = ab * launch_upd / (avg_int_ms * 1e-3) / 1e9 if int_n else None
-        roofline = {"bound": "hbm", "achieved": achieved_gbs, "peak": peak_gbs, "unit": "GB/s",
-                    "frac": (achieved_gbs / peak_gbs) if achieved_gbs else None, "traffic": traffic,
-                    "kernel": args.kernel, "kernel_ms_avg": avg_int_ms,
-                    "kernel_share_of_step": (int_ms / total_ms) if total_ms else None, "peak_source": peak_src,
-                    "algorithmic": f"{ab} B per spring update (SURVEY.md §8(d)) x {launch_upd} updates per launch",
-                    "fp64_pipe_busy_ncu": meta.get("fp64_pipe_pct")}
+        achieved = ab * upd_per_launch / (avg_int_ms * 1e-3) / 1e9 if int_n else None
+        roofline = {"bound": "hbm", "achieved": achieved, "peak": peak_gbs, "unit": "GB/s",
+                    "frac": (achieved / peak_gbs) if achieved else None, "traffic": traffic,
+                    "peak_source": peak_src,
+                    "algorithmic": f"{ab} B per spring update (SURVEY.md §8(d)) x {upd_per_launch:.4g} updates per "
+                                   "launch"}
     else:
-        roofline = {"bound": "fp64", "achieved": achieved_tf, "peak": peak_tf, "unit": "TFLOP/s",
-                    "frac": (achieved_tf / peak_tf) if achieved_tf else None, "traffic": traffic,
-                    "kernel": args.kernel, "kernel_ms_avg": avg_int_ms,
-                    "kernel_share_of_step": (int_ms / total_ms) if total_ms else None,
-                    "peak_source": "measured DFMA throughput on this GPU (vx_fp64_peak; MEASURED_PEAKS.json has no "
-                                   "FP64 entry), 2 flop/DFMA",
-                    "algorithmic": f"{FLOPS_PER_UPDATE} FP64 flop + 1 sqrt + 1 div per spring update x "
-                                   f"{local_upd} updates per launch",
-                    "fp64_pipe_busy_ncu": meta.get("fp64_pipe_pct"),
-                    "note": "parity mode forbids FMA contraction and IEEE sqrt/1/x cost ~15 FP64 instructions for 2 "
-                            "counted flop, so the flop fraction is structurally capped near 40%; fp64_pipe_busy_ncu "
-                            "is the FP64-pipe utilisation of the same kernel from the committed ncu capture"}
+        achieved = FLOPS_PER_UPDATE * upd_per_launch / (avg_int_ms * 1e-3) / 1e12 if int_n else None
+        peak = ctx.fp64_peak_tflops()
+        roofline = {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                    "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                    "peak_source": "measured DFMA throughput of this GPU (vx_fp64_peak, csrc/measure.cu; "
+                                   "MEASURED_PEAKS.json has no FP64 entry), 2 flop per DFMA",
+                    "algorithmic": f"{FLOPS_PER_UPDATE} FP64 flop + 1 sqrt + 1 div per spring update (SURVEY.md "
+                                   f"§8(d)) x {upd_per_launch:.4g} updates per launch",
+                    "note": "parity mode forbids FMA contraction and the IEEE sqrt / reciprocal cost ~15 FP64 "
+                            "instructions for 2 counted flop, so the flop fraction is structurally capped near 40%; "
+                            "fp64_pipe_busy_ncu is the FP64-pipe utilisation of the same kernel at the bench shape"}
+    roofline.update({"kernel": W["kernel"], "kernel_ms_avg": avg_int_ms, "launches_timed": int_n,
+                     "kernel_share_of_step": (int_ms / total_ms) if total_ms else None,
+                     "fp64_pipe_busy_ncu": meta.get("fp64_pipe_pct") if meta.get("workload") == args.workload
+                     else None,
+                     "ncu_source": meta.get("source")})
 
-    cpu = None
+    cpu = parity = None
     if world == 1 and not args.no_cpu_baseline and not args.profile:
-        pop = st.population()  # after the last step: elites keep grids -> re-decode for the sample
-        ns = min(P, CPU_SAMPLE_MAX if GRID <= 6 else 32)  # bounded: ~2-20 s of host work
-        mats, wts = vx.decode(init_params[:ns].cpu().numpy(), init_bmat[:ns].cpu().numpy(), st.config.arch, GRID,
-                              GRID, GRID, ctx)
-        upd, meta = cpu_baseline_sample(mats, wts)
-        cpu = {"value": (upd / meta["secs"]) if upd else None, "unit": "spring_updates/s", "cores": meta["cores"],
-               "kind": meta["kind"],
-               "sample": f"evaluate_fitness over {mats.shape[0]} of this config's decoded {GRID}^3 robots x "
-                         f"{SIM_STEPS} steps ({upd} updates) via the reference's parallel_for, {meta['secs']:.2f} s"}
-        del pop
-    h2d = P * (np_ + nb) * 8
-    d2h = P * 8 + P * 8 + 3 * 8 + 8 + 4
+        cpu, parity = cpu_baseline_and_parity(W, params0, bmat0, fit0)
     line = {
         "metric": METRIC, "value": value, "unit": "spring_updates/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": args.desc, "population": P, "grid": [GRID] * 3,
-                   "sim_steps": SIM_STEPS, "dt": DT, "seed": SEED, "l2": "flushed (256 MiB write) between steps",
-                   "parallelism": f"population shards x{world}"},
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": config_block(W, world),
         "generations_per_s": args.steps / (total_ms * 1e-3),
-        "spring_updates_per_step": upd_per_step,
+        "generations_timed": f"{args.warmup}..{args.warmup + args.steps - 1} (generation 0 = first warm-up step)",
+        "spring_updates_per_step": float(np.mean(upd)),
+        "spring_updates_timed": int(np.sum(upd)),
         "e2e": {"value": value_e2e, "unit": "spring_updates/s", "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h},
+                "d2h_bytes_per_step": d2h,
+                "what": f"generations {args.warmup + args.steps}..{args.warmup + 2 * args.steps - 1} with the "
+                        "population host-resident (pinned): upload + evolve_generation + download per step",
+                "generations_per_s": (len(ms_e2e) / (total_e2e * 1e-3)) if ms_e2e else None},
         "gpu_launches": int(launches),
         "roofline": roofline,
         "cpu_baseline": cpu,
+        "parity": parity,
         "clocks": clk.summary(),
         "vs_paper_rtx3090": value / 7892537853.0,
-        "best_fitness_gen0": reps[0].best,
+        "best_fitness": float(st.best()[0]),
     }
     print(json.dumps(line))
-    if distributed:
+    if comm is not None:
+        st.set_comm(None)
+        comm.close()
+    if launched:
         dist.destroy_process_group()
 
 
 def _ncu_json(name):
     """Figures from a committed ncu capture of the workload's integrator (profiles/*.json)."""
-    path = os.path.join(ROOT, "profiles", name)
     try:
-        return json.load(open(path))
+        return json.load(open(os.path.join(ROOT, "profiles", name)))
     except Exception:
         return {}
 

@@ -9,7 +9,7 @@
  *
  * Conventions
  *  - Status codes only; no exceptions cross the ABI.  vx_last_error() returns
- *    the calling thread's last message.  The C++ shim (voxevo_b200/voxevo.hpp)
+ *    the calling thread's last message.  The C++ shim (voxevo_b200/voxevo_shim.hpp)
  *    maps codes back to the reference exception types.
  *  - `_dev` entry points take DEVICE pointers (caller-owned, e.g. torch
  *    tensors) and are stream-ordered on the context stream (vx_set_stream);
@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define VX_ABI_VERSION 1
+#define VX_ABI_VERSION 2
 #define VX_MAX_HIDDEN 8
 #define VX_NMAT 5
 
@@ -41,12 +41,14 @@ typedef enum {
     VX_EEMPTY = 4,   /* empty_robot (morphology.hpp:17-19, :230) */
     VX_ESHAPE = 5,   /* shape_mismatch (genome.hpp:19-21) */
     VX_ESTATE = 6,   /* call made in the wrong state (e.g. finish before begin) */
-    VX_ENODEV = 7    /* no CUDA device / extension unusable */
+    VX_ENODEV = 7,   /* no CUDA device / extension unusable */
+    VX_ENCCL = 8     /* NCCL missing or failed (vx_comm_*) */
 } vx_status;
 
 typedef struct vx_ctx vx_ctx;     /* one per device: stream, scratch, counters */
 typedef struct vx_batch vx_batch; /* device-resident batch of MassSpringSystems */
 typedef struct vx_evo vx_evo;     /* device-resident EvolutionState */
+typedef struct vx_comm vx_comm;   /* NCCL communicator of one rank (one GPU) */
 
 /* EncodingSpec + hidden widths (genome.hpp:25-35, sample_genome :146) */
 typedef struct {
@@ -295,6 +297,38 @@ vx_status vx_evo_set_population(vx_evo* e, const double* params, const double* b
 /* Device views of the population genomes (P x np, P x 3m), valid until the
  * next vx_evo_* call. */
 vx_status vx_evo_population_dev(vx_evo* e, double** d_params, double** d_bmat, double** d_fitness);
+/* -------------------------------------- population sharding
+ * Replaces the CPU parallel_for over children (evolution.hpp:237-241,
+ * parallel.hpp:17-51) across GPUs: GA state replicated, children sharded,
+ * ONE sum all-reduce of the exchange buffer per generation; results are
+ * bit-identical for any world size (the reference's thread-count invariance,
+ * test_evolution.cpp:196-215).  NCCL is loaded at run time (libnccl.so.2). */
+#define VX_COMM_ID_BYTES 128
+vx_status vx_comm_available(void);                            /* VX_OK when NCCL is loadable */
+vx_status vx_comm_unique_id(uint8_t id[VX_COMM_ID_BYTES]);    /* rank 0 creates, the caller distributes */
+/* One process per GPU (ncclCommInitRank; collective over the `world` ranks). */
+vx_status vx_comm_create(vx_ctx* ctx, int32_t world, int32_t rank, const uint8_t id[VX_COMM_ID_BYTES],
+                         vx_comm** out);
+/* One process driving n GPUs (ncclCommInitAll over the contexts' devices). */
+vx_status vx_comm_create_all(int32_t n, vx_ctx* const* ctxs, vx_comm** comms);
+vx_status vx_comm_destroy(vx_comm* c);
+vx_status vx_comm_rank(const vx_comm* c, int32_t* rank, int32_t* world);
+/* Sum all-reduce of n device doubles on the communicator's context stream. */
+vx_status vx_comm_allreduce_sum_dev(vx_comm* c, double* d_buf, int64_t n);
+/* Attach a communicator: vx_evo_generation then runs begin(rank, world) ->
+ * all-reduce of the exchange buffer -> finish.  NULL detaches. */
+vx_status vx_evo_set_comm(vx_evo* e, vx_comm* c);
+/* Any other transport (MPI, gloo, host copies): vx_evo_generation calls
+ * fn(d_buf, n_doubles, user) between begin and finish; fn must leave the
+ * element-wise SUM over all ranks in d_buf (device memory, context stream
+ * synchronised before the call).  NULL detaches. */
+typedef vx_status (*vx_exchange_fn)(double* d_buf, int64_t n_doubles, void* user);
+vx_status vx_evo_set_exchange(vx_evo* e, int32_t rank, int32_t world, vx_exchange_fn fn, void* user);
+/* One host thread, n GPUs: every evo has a communicator from ONE
+ * vx_comm_create_all; begins all, all-reduces as one NCCL group, finishes
+ * all.  reps may be NULL. */
+vx_status vx_evo_generation_group(int32_t n, vx_evo* const* evos, vx_report* reps);
+
 /* Rng::state / set_state text form of the GA stream (rng.hpp:41-50). */
 int64_t vx_evo_rng_state(vx_evo* e, char* buf, int64_t cap);
 vx_status vx_evo_set_rng_state(vx_evo* e, const char* state);

@@ -131,6 +131,7 @@ class _Lib:
             f("evaluate_batch", C.c_double, [C.c_int, C.c_int, C.c_int, C.c_int, vp, vp, vp, vp, vp, C.c_int, vp,
                                              vp])
             f("evo_set_threads", None, [vp, C.c_int])
+            f("evo_generation_timed", C.c_double, [vp, vp, vp])
         else:
             f("simulate", None, [vp, vp, vp])
 
@@ -378,6 +379,15 @@ class Evo:
         return dict(generation=int(rep[0]), best=float(rep[1]), mean=float(rep[2]), stddev=float(rep[3]),
                     diversity=float(rep[4]), evaluations=int(rep[5]), wall_time=float(rep[6]),
                     params=rep[7:14].copy())
+
+    def generation_timed(self):
+        """(report, seconds of evolve_generation alone, exact spring updates it performed)."""
+        rep = np.zeros(14)
+        upd = np.zeros(1, np.uint64)
+        secs = self.lib._evo_generation_timed(self.h, rep.ctypes.data, upd.ctypes.data)
+        return dict(generation=int(rep[0]), best=float(rep[1]), mean=float(rep[2]), stddev=float(rep[3]),
+                    diversity=float(rep[4]), evaluations=int(rep[5]), wall_time=float(rep[6]),
+                    params=rep[7:14].copy()), float(secs), int(upd[0])
 
     def population(self) -> dict:
         P, np_, cells = self.P, self.np, self.cells

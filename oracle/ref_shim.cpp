@@ -437,6 +437,48 @@ void ref_evo_generation(void* h, double* rep) {
     rep[6] = r.wall_time;
     hyper_to(r.params, rep + 7);
 }
+// bench.py --impl reference: one evolve_generation (evolution.hpp:217-293)
+// timed alone; returns its wall seconds.  Afterwards, outside the timed
+// region, an exact audit of the spring updates it performed: the individuals
+// it had to evaluate (evaluated == false on entry) are decoded and evaluated
+// again with the reference's own functions (same code path, deterministic),
+// counting springs x steps exactly like simulate's ws.spring_updates
+// (physics.hpp:212).  rep as ref_evo_generation.
+double ref_evo_generation_timed(void* h, double* rep, uint64_t* updates) {
+    auto* e = static_cast<RefEvo*>(h);
+    std::vector<Genome> todo;
+    for (const auto& ind : e->st.population)
+        if (!ind.evaluated) todo.push_back(ind.genome);
+    const EvolutionConfig cfg = e->st.config;
+    const MaterialTable table = detail::scaled_materials(cfg.materials, e->st.params);
+    const auto t0 = std::chrono::steady_clock::now();
+    const GenerationReport r = evolve_generation(e->st);
+    const double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    rep[0] = r.generation;
+    rep[1] = r.best;
+    rep[2] = r.mean;
+    rep[3] = r.stddev;
+    rep[4] = r.diversity;
+    rep[5] = r.evaluations;
+    rep[6] = r.wall_time;
+    hyper_to(r.params, rep + 7);
+    std::vector<uint64_t> count(todo.size(), 0);
+    const long long n_steps = std::llround(cfg.sim.duration / cfg.sim.dt);
+    parallel_for(todo.size(), cfg.threads, [&](std::size_t a) {
+        VoxelGrid body = largest_component(decode(todo[a], cfg.grid_w, cfg.grid_h, cfg.grid_d));
+        if (body.count_non_empty() == 0 || !body.has_muscle()) return;
+        MassSpringSystem sys = build_mass_spring(body, table, cfg.plane);
+        SimWorkspace ws(sys);
+        for (long long k = 0; k < n_steps; ++k)
+            if (step(sys, static_cast<double>(k) * cfg.sim.dt, cfg.sim, ws) == StepResult::diverged) break;
+        count[a] = ws.spring_updates;
+    });
+    uint64_t total = 0;
+    for (uint64_t c : count) total += c;
+    if (updates) *updates = total;
+    return secs;
+}
+
 int ref_evo_generation_index(void* h) { return static_cast<RefEvo*>(h)->st.generation; }
 // Population export: params P x n_params, bmat P x 3m, fitness, evaluated,
 // raw grids P x cells (material 255 where the grid is not decoded yet).

@@ -26,7 +26,7 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "_lib", "libvoxevo_b200.so")
 
-VX_OK, VX_EINVAL, VX_ECUDA, VX_EOOM, VX_EEMPTY, VX_ESHAPE, VX_ESTATE, VX_ENODEV = range(8)
+VX_OK, VX_EINVAL, VX_ECUDA, VX_EOOM, VX_EEMPTY, VX_ESHAPE, VX_ESTATE, VX_ENODEV, VX_ENCCL = range(9)
 NMAT = 5
 MAX_HIDDEN = 8
 
@@ -198,7 +198,7 @@ def _lib():
                 "there is no CPU fallback")
         lib = C.CDLL(LIB_PATH)
         _declare(lib)
-        if lib.vx_abi_version() != 1:
+        if lib.vx_abi_version() != 2:
             raise DeviceUnavailable("libvoxevo_b200 ABI mismatch")
         _LIB = lib
     return _LIB
@@ -289,6 +289,16 @@ def _declare(lib):
         "vx_crossover": (i32, [vp, i64, vp, vp, vp]),
         "vx_mutate": (i32, [vp, i64, vp, dbl, dbl]),
         "vx_tournament_select": (i32, [vp, i32, i32]),
+        "vx_comm_available": (i32, []),
+        "vx_comm_unique_id": (i32, [vp]),
+        "vx_comm_create": (i32, [vp, i32, i32, vp, P(vp)]),
+        "vx_comm_create_all": (i32, [i32, vp, vp]),
+        "vx_comm_destroy": (i32, [vp]),
+        "vx_comm_rank": (i32, [vp, P(i32), P(i32)]),
+        "vx_comm_allreduce_sum_dev": (i32, [vp, vp, i64]),
+        "vx_evo_set_comm": (i32, [vp, vp]),
+        "vx_evo_set_exchange": (i32, [vp, i32, i32, vp, vp]),
+        "vx_evo_generation_group": (i32, [i32, vp, vp]),
     }
     for name, (res, args) in sigs.items():
         fn = getattr(lib, name)
@@ -317,6 +327,8 @@ def _check(st: int, what: str = ""):
         raise ShapeMismatch(text)
     if st == VX_ENODEV:
         raise DeviceUnavailable(text)
+    if st == VX_ENCCL:
+        raise VoxevoError(f"NCCL: {text}")
     raise VoxevoError(f"status {st}: {text}")
 
 
@@ -832,6 +844,18 @@ class EvolutionState:
                                                       ("params", "bmat", "fitness", "evaluated", "grids", "grid_w")]))
         return out
 
+    def get_population_into(self, params, bmat, fitness=None, evaluated=None):
+        """Copy the population into caller arrays (e.g. pinned host memory):
+        params (P, np) f64, bmat (P, 3m) f64, fitness (P,) f64, evaluated (P,) u8."""
+        P = self.config.population
+        checks = [(params, (P, self.np), np.float64), (bmat, (P, 3 * self.config.arch.m), np.float64),
+                  (fitness, (P,), np.float64), (evaluated, (P,), np.uint8)]
+        for a, shape, dt in checks:
+            if a is not None and (a.shape != shape or a.dtype != dt or not a.flags.c_contiguous):
+                raise ValueError(f"get_population_into: expected a C-contiguous {dt.__name__} array of shape {shape}")
+        _check(_lib().vx_evo_get_population(self.h, _ptr(params), _ptr(bmat), _ptr(fitness), _ptr(evaluated), None,
+                                            None), "get_population")
+
     def set_population(self, params, bmat, fitness=None, evaluated=None, grids=None, grid_w=None):
         c = np.ascontiguousarray
         arrs = [c(params, np.float64), c(bmat, np.float64), None if fitness is None else c(fitness, np.float64),
@@ -878,6 +902,83 @@ class EvolutionState:
         _check(_lib().vx_evo_finish(self.h, C.byref(rep)), "evo_finish")
         self.history.append(rep)
         return rep
+
+    def set_comm(self, comm: Optional["Communicator"]):
+        """Shard every evolve_generation over the communicator's ranks (NCCL
+        all-reduce of the exchange buffer inside the library)."""
+        self._comm = comm
+        _check(_lib().vx_evo_set_comm(self.h, comm.h if comm is not None else None), "set_comm")
+
+    def set_exchange(self, rank: int, world: int, fn: Optional[Callable[[int, int], None]]):
+        """Shard over any transport: fn(d_buf_ptr, n_doubles) must leave the
+        element-wise sum over all ranks in the device buffer."""
+        if fn is None:
+            self._xfn = None
+            _check(_lib().vx_evo_set_exchange(self.h, 0, 1, None, None), "set_exchange")
+            return
+
+        def tramp(d_buf, n, _user):
+            try:
+                fn(int(d_buf or 0), int(n))
+                return VX_OK
+            except Exception:  # reported as a CUDA-side failure of the exchange
+                return VX_ECUDA
+        self._xfn = _EXCHANGE_FN(tramp)
+        _check(_lib().vx_evo_set_exchange(self.h, rank, world, self._xfn, None), "set_exchange")
+
+
+_EXCHANGE_FN = C.CFUNCTYPE(C.c_int32, C.c_void_p, C.c_int64, C.c_void_p)
+
+
+def _nccl_lib():
+    """The library resolves NCCL at first use and prefers one already in the
+    process: make that PyTorch's (importing torch after the system NCCL was
+    loaded would bind torch to the older copy)."""
+    try:
+        import torch  # noqa: F401
+    except ImportError:
+        pass
+    return _lib()
+
+
+class Communicator:
+    """NCCL communicator of one rank (vx_comm_create): population sharding
+    across GPUs, one process per GPU."""
+
+    @staticmethod
+    def available() -> bool:
+        return _nccl_lib().vx_comm_available() == VX_OK
+
+    @staticmethod
+    def unique_id() -> bytes:
+        _nccl_lib()
+        buf = (C.c_uint8 * 128)()
+        _check(_lib().vx_comm_unique_id(buf), "comm_unique_id")
+        return bytes(buf)
+
+    def __init__(self, ctx: "Context", world: int, rank: int, uid: bytes):
+        if len(uid) != 128:
+            raise ValueError("NCCL unique id must be 128 bytes")
+        self.ctx = ctx
+        buf = (C.c_uint8 * 128).from_buffer_copy(uid)
+        h = C.c_void_p()
+        _check(_lib().vx_comm_create(ctx.h, world, rank, buf, C.byref(h)), "comm_create")
+        self.h = h
+        self.rank, self.world = rank, world
+
+    def allreduce_sum_dev(self, d_ptr: int, n: int):
+        _check(_lib().vx_comm_allreduce_sum_dev(self.h, d_ptr, n), "comm_allreduce")
+
+    def close(self):
+        if getattr(self, "h", None):
+            _lib().vx_comm_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def shard_indices(todo: Sequence[int], rank: int, world: int) -> list:

@@ -387,6 +387,14 @@ vx_status forward_dev(vx_ctx* ctx, const vx_arch* a, int P, const double* d_para
     return launch_decode(ctx, a, np, maxw, A, P);
 }
 
+vx_status decode_feasible(vx_ctx* ctx, const vx_arch* a) {
+    int maxw = 2 * a->m;
+    for (int l = 0; l < a->n_hidden; ++l) maxw = maxw > a->hidden[l] ? maxw : a->hidden[l];
+    const size_t act = (2ull * maxw + VX_NMAT + 1) * kTile * sizeof(double) + 3ull * a->m * sizeof(double);
+    if (act > ctx->smem_optin) return (set_error("decode: architecture too wide"), VX_EINVAL);
+    return VX_OK;
+}
+
 vx_status launch_decode(vx_ctx* ctx, const vx_arch* a, int64_t np, int maxw, DecodeArgs& A, int n) {
     const size_t act = (2ull * maxw + VX_NMAT + 1) * kTile * sizeof(double) + 3ull * a->m * sizeof(double);
     size_t smem = act + static_cast<size_t>(np) * sizeof(double);

@@ -100,6 +100,10 @@ struct vx_evo {
     bool plan_running = false;
     bool plan_failed = false;  // host allocation failed inside the plan thread
     std::mt19937_64 rng;
+    // begin() snapshot for rolling a generation back
+    std::mt19937_64 rng_at_begin;
+    std::vector<uint8_t> has_grid_at_begin;
+    std::vector<int32_t> owner_at_begin;
     int generation = 0;
     double best_fitness = 0.0;
     bool has_best = false;
@@ -112,6 +116,12 @@ struct vx_evo {
     vx_materials table{};
     double* ext_xbuf = nullptr;  // caller-owned exchange buffer (NCCL all-reduce operand)
     double* xb() { return ext_xbuf ? ext_xbuf : xbuf.p; }
+    // the exchange step of vx_evo_generation: an NCCL communicator, or a
+    // caller transport (rank / world of the shard either way)
+    vx_comm* comm = nullptr;
+    vx_exchange_fn xfn = nullptr;
+    void* xuser = nullptr;
+    int x_rank = 0, x_world = 1;
 
     ~vx_evo() {
         if (plan_thread.joinable()) plan_thread.join();
@@ -204,6 +214,17 @@ void join_plan(vx_evo* e) {
     e->plan_running = false;
 }
 
+// a begun generation whose exchange failed: join the plan and restore the
+// state begin() found (RNG position, grid ownership)
+void abandon_generation(vx_evo* e) {
+    join_plan(e);
+    cudaStreamSynchronize(e->ctx->stream);
+    e->rng = e->rng_at_begin;
+    e->h_has_grid = e->has_grid_at_begin;
+    e->h_owner = e->owner_at_begin;
+    e->begun = false;
+}
+
 }  // namespace
 
 extern "C" {
@@ -211,6 +232,7 @@ extern "C" {
 vx_status vx_evo_create(vx_ctx* ctx, const vx_evo_config* cfg, vx_evo** out) {
     if (!ctx || !cfg || !out) return VX_EINVAL;
     VX_TRY(validate_cfg(cfg));
+    VX_TRY(decode_feasible(ctx, &cfg->arch));  // fail up front, not in a later generation
     auto e = std::make_unique<vx_evo>();
     e->ctx = ctx;
     e->cfg = *cfg;
@@ -246,9 +268,28 @@ vx_status vx_evo_free(vx_evo* e) {
     return VX_OK;
 }
 
+namespace {
+vx_status evo_begin_body(vx_evo* e, int32_t rank, int32_t world);
+}
+
 vx_status vx_evo_begin(vx_evo* e, int32_t rank, int32_t world) {
     if (!e || world < 1 || rank < 0 || rank >= world) return VX_EINVAL;
     if (e->begun) return (set_error("vx_evo_begin: generation already begun"), VX_ESTATE);
+    join_plan(e);  // never assign a new plan thread over a joinable one
+    // a failed begin leaves the state as it found it: RNG position, grid
+    // ownership and the plan thread (joined) all rolled back
+    e->rng_at_begin = e->rng;
+    e->has_grid_at_begin = e->h_has_grid;
+    e->owner_at_begin = e->h_owner;
+    const vx_status s = evo_begin_body(e, rank, world);
+    if (s != VX_OK) abandon_generation(e);
+    return s;
+}
+
+}  // extern "C"
+
+namespace {
+vx_status evo_begin_body(vx_evo* e, int32_t rank, int32_t world) {
     vx_ctx* ctx = e->ctx;
     e->t0 = std::chrono::steady_clock::now();
     e->rank = rank;
@@ -324,6 +365,9 @@ vx_status vx_evo_begin(vx_evo* e, int32_t rank, int32_t world) {
     e->begun = true;
     return VX_OK;
 }
+}  // namespace
+
+extern "C" {
 
 vx_status vx_evo_exchange_buffer(vx_evo* e, double** d_buf, int64_t* n_doubles) {
     if (!e || !d_buf) return VX_EINVAL;
@@ -465,8 +509,76 @@ vx_status vx_evo_finish(vx_evo* e, vx_report* rep) {
 }
 
 vx_status vx_evo_generation(vx_evo* e, vx_report* rep) {
+    if (!e) return VX_EINVAL;
+    if (e->comm) {  // sharded over the communicator's ranks
+        VX_TRY(vx_evo_begin(e, comm_rank(e->comm), comm_world(e->comm)));
+        const vx_status s = comm_exchange(e->comm, e->xb(), static_cast<int64_t>(xbuf_doubles(e)));
+        if (s != VX_OK) {
+            abandon_generation(e);
+            return s;
+        }
+        return vx_evo_finish(e, rep);
+    }
+    if (e->xfn) {
+        VX_TRY(vx_evo_begin(e, e->x_rank, e->x_world));
+        cudaError_t ce = cudaStreamSynchronize(e->ctx->stream);
+        const vx_status s = ce != cudaSuccess ? cuda_status(ce, "exchange")
+                                              : e->xfn(e->xb(), static_cast<int64_t>(xbuf_doubles(e)), e->xuser);
+        if (s != VX_OK) {
+            abandon_generation(e);
+            return s;
+        }
+        return vx_evo_finish(e, rep);
+    }
     VX_TRY(vx_evo_begin(e, 0, 1));
     return vx_evo_finish(e, rep);
+}
+
+vx_status vx_evo_set_comm(vx_evo* e, vx_comm* c) {
+    if (!e) return VX_EINVAL;
+    if (e->begun) return (set_error("communicator change mid-generation"), VX_ESTATE);
+    if (c && comm_ctx(c)->device != e->ctx->device)
+        return (set_error("vx_evo_set_comm: communicator and evolution state are on different devices"), VX_EINVAL);
+    e->comm = c;
+    return VX_OK;
+}
+
+vx_status vx_evo_set_exchange(vx_evo* e, int32_t rank, int32_t world, vx_exchange_fn fn, void* user) {
+    if (!e || (fn && (world < 1 || rank < 0 || rank >= world))) return VX_EINVAL;
+    if (e->begun) return (set_error("exchange change mid-generation"), VX_ESTATE);
+    e->xfn = fn;
+    e->xuser = user;
+    e->x_rank = fn ? rank : 0;
+    e->x_world = fn ? world : 1;
+    return VX_OK;
+}
+
+vx_status vx_evo_generation_group(int32_t n, vx_evo* const* evos, vx_report* reps) {
+    if (n < 1 || !evos) return VX_EINVAL;
+    std::vector<vx_comm*> cs(static_cast<size_t>(n));
+    std::vector<double*> bufs(static_cast<size_t>(n));
+    std::vector<int64_t> counts(static_cast<size_t>(n));
+    for (int i = 0; i < n; ++i) {
+        if (!evos[i] || !evos[i]->comm || comm_world(evos[i]->comm) != n)
+            return (set_error("vx_evo_generation_group: every state needs a communicator of this group"), VX_EINVAL);
+        cs[static_cast<size_t>(i)] = evos[i]->comm;
+    }
+    int begun = 0;
+    vx_status s = VX_OK;
+    for (; begun < n && s == VX_OK; ++begun) {
+        vx_evo* e = evos[begun];
+        s = vx_evo_begin(e, comm_rank(e->comm), n);
+        if (s != VX_OK) break;
+        bufs[static_cast<size_t>(begun)] = e->xb();
+        counts[static_cast<size_t>(begun)] = static_cast<int64_t>(xbuf_doubles(e));
+    }
+    if (s == VX_OK) s = comm_exchange_group(n, cs.data(), bufs.data(), counts.data());
+    if (s != VX_OK) {
+        for (int i = 0; i < begun; ++i) abandon_generation(evos[i]);
+        return s;
+    }
+    for (int i = 0; i < n; ++i) VX_TRY(vx_evo_finish(evos[i], reps ? reps + i : nullptr));
+    return VX_OK;
 }
 
 vx_status vx_evo_get_population(vx_evo* e, double* params, double* bmat, double* fitness, uint8_t* evaluated,

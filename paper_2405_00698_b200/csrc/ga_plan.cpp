@@ -170,10 +170,19 @@ uint64_t u01_threshold(double p) {
 }
 
 // Normals of full chunks, computed by a small pool while the scan runs on.
+// Workers see a chunk only through the job copied out under `mu`: the scan
+// thread keeps growing MutStore's vectors (which may reallocate) and its
+// entry count, so no worker ever reads MutStore's members.
+struct NormalJob {
+    MutEntry* e;
+    const uint64_t* r2;
+    size_t count;
+};
 struct NormalPool {
     std::mutex mu;
     std::condition_variable cv;
-    size_t published = 0, claimed = 0;  // chunks ready / taken
+    std::vector<NormalJob> jobs;  // published chunks, in order
+    size_t claimed = 0;           // jobs taken
     bool done = false;
     std::vector<std::thread> threads;
 };
@@ -185,10 +194,10 @@ struct MutWriter {
     NormalPool& pool;
     double scale;
 
-    void fill_chunk(size_t j, size_t count) {
-        MutEntry* e = st.e_[j];
-        const uint64_t* r2 = st.r2_[j];
-        for (size_t q = 0; q < count; ++q) {
+    void fill_chunk(const NormalJob& job) {
+        MutEntry* e = job.e;
+        const uint64_t* r2 = job.r2;
+        for (size_t q = 0; q < job.count; ++q) {
             uint64_t r1;
             std::memcpy(&r1, &e[q].delta, sizeof(r1));
             e[q].delta = box_muller(r1, r2[q]) * scale;
@@ -197,14 +206,14 @@ struct MutWriter {
     // claim chunks until the scan is over and every chunk is taken
     void work() {
         for (;;) {
-            size_t j;
+            NormalJob job;
             {
                 std::unique_lock<std::mutex> lk(pool.mu);
-                pool.cv.wait(lk, [&] { return pool.claimed < pool.published || pool.done; });
-                if (pool.claimed >= pool.published) return;  // done
-                j = pool.claimed++;
+                pool.cv.wait(lk, [&] { return pool.claimed < pool.jobs.size() || pool.done; });
+                if (pool.claimed >= pool.jobs.size()) return;  // done
+                job = pool.jobs[pool.claimed++];
             }
-            fill_chunk(j, st.chunk_size(j));
+            fill_chunk(job);
         }
     }
     inline void append(int32_t c, int32_t i, uint64_t r1, uint64_t r2) {
@@ -216,13 +225,16 @@ struct MutWriter {
         std::memcpy(&m.delta, &r1, sizeof(r1));
         st.r2_[j][k] = r2;
         ++st.n_;
-        if (k + 1 == MutStore::kChunk) {
-            {
-                std::lock_guard<std::mutex> lk(pool.mu);
-                pool.published = j + 1;
-            }
-            pool.cv.notify_one();
+        if (k + 1 == MutStore::kChunk) publish(j);
+    }
+    // hand chunk j (complete: no more appends to it) to the workers
+    void publish(size_t j) {
+        const NormalJob job{st.e_[j], st.r2_[j], st.chunk_size(j)};
+        {
+            std::lock_guard<std::mutex> lk(pool.mu);
+            pool.jobs.push_back(job);
         }
+        pool.cv.notify_one();
     }
     void grow() {  // a slab as large as everything so far (1..256 chunks): few, large pinned allocations
         const size_t n = std::min<size_t>(256, std::max<size_t>(1, st.e_.size()));
@@ -384,9 +396,9 @@ void plan_scan(std::mt19937_64& rng, const PlanParams& a, std::vector<ChildPlan>
         scan_body(*s, kern, a, o);
         store(*s, rng);
     }
+    if (mut.size() % MutStore::kChunk != 0) w.publish(mut.chunks() - 1);  // the partial tail chunk
     {
         std::lock_guard<std::mutex> lk(pool.mu);
-        pool.published = mut.chunks();
         pool.done = true;
     }
     pool.cv.notify_all();
