@@ -218,6 +218,11 @@ vx_status vx_batch_override_phase(vx_batch* b, const double* sin_phase, const do
  * max_speed, steps and exact spring updates of THIS call. */
 vx_status vx_batch_step(vx_ctx* ctx, vx_batch* b, const vx_sim* sim, int64_t k0, int64_t n_steps,
                         vx_summary* summaries);
+/* step(sys, t, cfg, ws) (physics.hpp:191-264) once on every robot at an
+ * arbitrary time t (drive sin/cos((2 pi f) t) with the host libm); MUTATES
+ * the batch state; summaries as vx_batch_step (steps = 1 unless diverged,
+ * spring_updates = springs when phase 1 completed). */
+vx_status vx_batch_step_at(vx_ctx* ctx, vx_batch* b, const vx_sim* sim, double t, vx_summary* summaries);
 /* simulate() (physics.hpp:287-311) for every robot: llround(duration/dt)
  * steps from t = 0 on a private copy of the state (the batch is not
  * modified, like the reference's by-value argument). */
@@ -291,7 +296,9 @@ vx_status vx_evo_load_population_dev(vx_evo* e, const double* d_params, const do
 vx_status vx_evo_finish(vx_evo* e, vx_report* rep);
 vx_status vx_evo_get_population(vx_evo* e, double* params, double* bmat, double* fitness, uint8_t* evaluated,
                                 uint8_t* grids, double* grid_w);
-/* Replace the population (host arrays).  grids NULL => not decoded yet. */
+/* Replace the population (host arrays).  grids NULL => not decoded yet; with
+ * grids, an individual whose first cell holds material 255 (the marker
+ * vx_evo_get_population writes) is not decoded yet either. */
 vx_status vx_evo_set_population(vx_evo* e, const double* params, const double* bmat, const double* fitness,
                                 const uint8_t* evaluated, const uint8_t* grids, const double* grid_w);
 /* Device views of the population genomes (P x np, P x 3m), valid until the

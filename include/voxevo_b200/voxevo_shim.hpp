@@ -3,21 +3,32 @@
 //
 // Include AFTER the reference headers (it uses voxevo::EvolutionConfig,
 // VoxelGrid, MassSpringSystem, ... unchanged).  Entry points mirror the
-// reference's names and semantics:
+// reference's names, signatures and semantics:
+//   voxevo::b200::sample_genome     <- voxevo::sample_genome     (genome.hpp:146)
+//   voxevo::b200::gaussian_encode   <- voxevo::gaussian_encode   (genome.hpp:169)
+//   voxevo::b200::forward           <- voxevo::forward           (genome.hpp:187)
 //   voxevo::b200::decode            <- voxevo::decode            (morphology.hpp:141)
 //   voxevo::b200::largest_component <- voxevo::largest_component (morphology.hpp:162)
 //   voxevo::b200::build_mass_spring <- voxevo::build_mass_spring (morphology.hpp:217)
+//   voxevo::b200::step              <- voxevo::step              (physics.hpp:191)
 //   voxevo::b200::simulate          <- voxevo::simulate          (physics.hpp:287)
 //   voxevo::b200::evaluate_fitness  <- voxevo::evaluate_fitness  (evolution.hpp:110)
-//   voxevo::b200::population_diversity <- (evolution.hpp:89)
-//   voxevo::b200::GpuEvolution      <- init_evolution / evolve_generation (evolution.hpp:197-293)
+//   voxevo::b200::population_diversity <- voxevo::population_diversity (evolution.hpp:89)
+//   voxevo::b200::crossover / mutate / tournament_select
+//                                   <- voxevo::detail::*         (evolution.hpp:143-173)
+//   voxevo::b200::init_evolution    <- voxevo::init_evolution    (evolution.hpp:197)
+//   voxevo::b200::evolve_generation <- voxevo::evolve_generation (evolution.hpp:217)
+//   voxevo::b200::GpuEvolution      device-resident EvolutionState (one GPU, or
+//                                   a rank of a sharded run: Communicator)
 //   voxevo::b200::run_bench         <- voxevo::run_bench         (bench.hpp:50)
 // Errors map back to the reference's exception types.
 #pragma once
 
-#include <optional>
 #include <algorithm>
 #include <cmath>
+#include <cstdint>
+#include <functional>
+#include <optional>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -53,7 +64,13 @@ inline Device& default_device() {
     return d;
 }
 
+inline void check_depth(std::size_t n_hidden) {
+    if (n_hidden > VX_MAX_HIDDEN)
+        throw std::invalid_argument("voxevo_b200: at most " + std::to_string(VX_MAX_HIDDEN) + " hidden layers");
+}
+
 inline vx_arch to_c(const Genome& g) {
+    check_depth(g.hidden.size());
     vx_arch a{};
     a.m = static_cast<int32_t>(g.spec.m);
     a.sigma = g.spec.sigma;
@@ -82,6 +99,7 @@ inline HyperParams from_c(const vx_hyper& h) {
     return p;
 }
 inline vx_evo_config to_c(const EvolutionConfig& c) {
+    check_depth(c.hidden_widths.size());
     vx_evo_config x;
     vx_default_evo_config(&x);
     x.population = c.population;
@@ -131,6 +149,41 @@ inline Genome unflatten(const EvolutionConfig& cfg, const double* params, const 
     g.head_material = layer(prev, 5);
     g.head_weight = layer(prev, 1);
     return g;
+}
+
+inline Genome unflatten(const EncodingSpec& spec, const std::vector<std::size_t>& hidden, const double* params,
+                        const double* bmat) {
+    EvolutionConfig c;
+    c.encoding = spec;
+    c.hidden_widths = hidden;
+    return unflatten(c, params, bmat);
+}
+
+// sample_genome (genome.hpp:146-166): the genome's own mt19937_64 stream;
+// layer weights drawn on device (exact uniforms), B with the host glibc
+// Box-Muller — bit-identical to the reference.
+inline Genome sample_genome(const EncodingSpec& spec, const std::vector<std::size_t>& hidden_widths,
+                            std::uint64_t seed, Device& dev = default_device()) {
+    spec.validate();
+    for (std::size_t w : hidden_widths)
+        if (w < 1) throw std::invalid_argument("sample_genome: hidden widths must be >= 1");
+    check_depth(hidden_widths.size());
+    vx_arch a{};
+    a.m = static_cast<int32_t>(spec.m);
+    a.sigma = spec.sigma;
+    a.n_hidden = static_cast<int32_t>(hidden_widths.size());
+    for (std::size_t i = 0; i < hidden_widths.size(); ++i) a.hidden[i] = static_cast<int32_t>(hidden_widths[i]);
+    std::vector<double> params(static_cast<std::size_t>(vx_param_count(&a))), bmat(3 * spec.m);
+    check(vx_sample_genomes(dev.get(), &a, 1, &seed, params.data(), bmat.data()));
+    return unflatten(spec, hidden_widths, params.data(), bmat.data());
+}
+
+// gaussian_encode (genome.hpp:169-179): host libm, bit-identical.
+inline std::vector<double> gaussian_encode(const Vec3& v, const std::vector<double>& b_matrix, std::size_t m) {
+    std::vector<double> out(2 * m);
+    const double p[3] = {v[0], v[1], v[2]};
+    check(vx_gaussian_encode(p, b_matrix.data(), static_cast<int32_t>(m), out.data()));
+    return out;
 }
 
 // forward (genome.hpp:187-211) for a batch of query points of one genome
@@ -227,14 +280,10 @@ inline MassSpringSystem build_mass_spring(const VoxelGrid& grid, const MaterialT
     return sys;
 }
 
-// simulate (physics.hpp:280-311), including the optional COM dump every
-// `stride` steps; the system is taken by value like the reference's.
-inline TrajectorySummary simulate(const MassSpringSystem& sys, const SimConfig& cfg,
-                                  std::vector<TrajectorySample>* dump = nullptr, int stride = 0,
-                                  Device& dev = default_device()) {
-    cfg.validate();
-    TrajectorySummary out;
-    if (sys.masses.empty()) return out;
+// A one-robot device batch holding `sys`, with the actuation phases'
+// sin/cos taken from the host libm exactly as SimWorkspace computes them
+// (physics.hpp:154-159), so the device integrator is bit-identical.
+inline vx_batch* upload_system(const MassSpringSystem& sys, Device& dev) {
     const int64_t nm = static_cast<int64_t>(sys.masses.size()), ns = static_cast<int64_t>(sys.springs.size());
     const int64_t mo[2] = {0, nm}, so[2] = {0, ns};
     std::vector<double> pos(3 * nm), vel(3 * nm), mass(nm), k(ns), rest0(ns), zeta(ns), sign(ns), amp(ns), phase(ns);
@@ -263,6 +312,59 @@ inline TrajectorySummary simulate(const MassSpringSystem& sys, const SimConfig& 
     vx_batch* b = nullptr;
     check(vx_batch_upload(dev.get(), 1, mo, so, pos.data(), vel.data(), mass.data(), si.data(), sj.data(), k.data(),
                           rest0.data(), zeta.data(), act.data(), sign.data(), amp.data(), phase.data(), &p, &b));
+    std::vector<double> sph(ns), cph(ns);
+    for (int64_t q = 0; q < ns; ++q) {
+        const Spring& sp = sys.springs[q];
+        sph[q] = sp.act ? std::sin(sp.act->phase) : 0.0;
+        cph[q] = sp.act ? std::cos(sp.act->phase) : 1.0;
+    }
+    const vx_status st = vx_batch_override_phase(b, sph.data(), cph.data());
+    if (st != VX_OK) {
+        vx_batch_free(b);
+        check(st);
+    }
+    return b;
+}
+
+// step (physics.hpp:191-264): one step of `sys` at time t on the device,
+// bit-identical to the reference's; the workspace's counters are updated
+// like the reference's (spring_updates += ns once phase 1 completes,
+// max_speed_sq over the new velocities).
+inline StepResult step(MassSpringSystem& sys, double t, const SimConfig& cfg, SimWorkspace& ws,
+                       Device& dev = default_device()) {
+    if (sys.masses.empty()) return StepResult::ok;
+    vx_batch* b = upload_system(sys, dev);
+    const vx_sim s = to_c(cfg);
+    vx_summary sum{};
+    const int64_t nm = static_cast<int64_t>(sys.masses.size());
+    std::vector<double> pos(3 * nm), vel(3 * nm);
+    vx_status st = vx_batch_step_at(dev.get(), b, &s, t, &sum);
+    if (st == VX_OK)
+        st = vx_batch_download(b, pos.data(), vel.data(), nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
+                               nullptr, nullptr, nullptr, nullptr);
+    vx_batch_free(b);
+    check(st);
+    ws.spring_updates += sum.spring_updates;
+    if (sum.spring_updates == 0 && !sys.springs.empty()) return StepResult::diverged;  // zero-length: untouched
+    for (int64_t a = 0; a < nm; ++a) {
+        PointMass& m = sys.masses[a];
+        m.pos = {pos[3 * a], pos[3 * a + 1], pos[3 * a + 2]};
+        m.vel = {vel[3 * a], vel[3 * a + 1], vel[3 * a + 2]};
+        const double speed_sq = m.vel[0] * m.vel[0] + m.vel[1] * m.vel[1] + m.vel[2] * m.vel[2];
+        if (speed_sq > ws.max_speed_sq) ws.max_speed_sq = speed_sq;
+    }
+    return sum.diverged ? StepResult::diverged : StepResult::ok;
+}
+
+// simulate (physics.hpp:280-311), including the optional COM dump every
+// `stride` steps; the system is taken by value like the reference's.
+inline TrajectorySummary simulate(const MassSpringSystem& sys, const SimConfig& cfg,
+                                  std::vector<TrajectorySample>* dump = nullptr, int stride = 0,
+                                  Device& dev = default_device()) {
+    cfg.validate();
+    TrajectorySummary out;
+    if (sys.masses.empty()) return out;
+    vx_batch* b = upload_system(sys, dev);
     const vx_sim s = to_c(cfg);
     vx_summary sum{};
     vx_status st;
@@ -315,6 +417,119 @@ inline double evaluate_fitness(const VoxelGrid& raw, const MaterialTable& table,
     return evaluate_fitness(std::vector<VoxelGrid>{raw}, table, plane, sim, dev)[0];
 }
 
+// population_diversity (evolution.hpp:89-105) over the raw grids (material
+// histogram per cell on device: exact integer counts, result within 1e-13 of
+// the reference's sequential per-pair sum).
+inline double population_diversity(const std::vector<Individual>& pop, Device& dev = default_device()) {
+    if (pop.size() < 2) return 0.0;
+    const std::size_t cells = pop[0].grid.cells.size();
+    if (cells == 0) return 0.0;
+    std::vector<uint8_t> mat;
+    mat.reserve(pop.size() * cells);
+    for (const auto& ind : pop) {
+        if (ind.grid.cells.size() != cells) throw std::invalid_argument("population_diversity: grids differ in size");
+        for (const auto& c : ind.grid.cells) mat.push_back(static_cast<uint8_t>(c.material));
+    }
+    double out = 0.0;
+    check(vx_population_diversity(dev.get(), static_cast<int32_t>(pop.size()), static_cast<int32_t>(cells), mat.data(),
+                                  &out));
+    return out;
+}
+
+// The GA operators on the CALLER's voxevo::Rng (evolution.hpp:143-173,
+// detail::crossover / mutate / tournament_select): the library's host
+// mt19937_64 continues the caller's stream from its text state and hands it
+// back, so draws, decisions and noise are bit-identical.
+class RngBridge {
+  public:
+    explicit RngBridge(Rng& rng) : rng_(rng) {
+        check(vx_rng_create(0, &r_));
+        const std::string st = rng.state();
+        const vx_status s = vx_rng_set_state(r_, st.c_str());
+        if (s != VX_OK) {
+            vx_rng_free(r_);
+            check(s);
+        }
+    }
+    ~RngBridge() {
+        std::string st(static_cast<std::size_t>(vx_rng_state(r_, nullptr, 0)), '\0');
+        vx_rng_state(r_, st.data(), static_cast<int64_t>(st.size()) + 1);
+        rng_.set_state(st);
+        vx_rng_free(r_);
+    }
+    RngBridge(const RngBridge&) = delete;
+    RngBridge& operator=(const RngBridge&) = delete;
+    vx_rng* get() const { return r_; }
+
+  private:
+    Rng& rng_;
+    vx_rng* r_ = nullptr;
+};
+
+inline Genome crossover(const Genome& a, const Genome& b, Rng& rng) {
+    if (!a.same_architecture(b)) throw shape_mismatch("crossover: parents differ in architecture");
+    std::vector<double> pa, pb;
+    flatten(a, pa);
+    flatten(b, pb);
+    std::vector<double> child(pa.size());
+    {
+        RngBridge r(rng);
+        check(vx_crossover(r.get(), static_cast<int64_t>(pa.size()), pa.data(), pb.data(), child.data()));
+    }
+    Genome g = a;  // B and the architecture from parent a
+    const double* p = child.data();
+    for (auto* t : g.param_tensors()) {
+        std::copy(p, p + t->size(), t->begin());
+        p += t->size();
+    }
+    return g;
+}
+
+inline void mutate(Genome& g, double rate, double scale, Rng& rng) {
+    std::vector<double> params;
+    flatten(g, params);
+    {
+        RngBridge r(rng);
+        check(vx_mutate(r.get(), static_cast<int64_t>(params.size()), params.data(), rate, scale));
+    }
+    const double* p = params.data();
+    for (auto* t : g.param_tensors()) {
+        std::copy(p, p + t->size(), t->begin());
+        p += t->size();
+    }
+}
+
+inline const Individual& tournament_select(const std::vector<Individual>& pop, int size, Rng& rng) {
+    RngBridge r(rng);
+    const int32_t w = vx_tournament_select(r.get(), static_cast<int32_t>(pop.size()), size);
+    if (w < 0) check(VX_EINVAL);
+    return pop[static_cast<std::size_t>(w)];
+}
+
+// One rank's NCCL communicator (vx_comm_create): rank 0 calls unique_id()
+// and distributes the 128 bytes (MPI, a file, a socket ...), every rank of
+// the world then constructs its Communicator with them (collective).
+class Communicator {
+  public:
+    using Id = std::vector<uint8_t>;
+    static Id unique_id() {
+        Id id(VX_COMM_ID_BYTES);
+        check(vx_comm_unique_id(id.data()));
+        return id;
+    }
+    Communicator(int world, int rank, const Id& id, Device& dev = default_device()) {
+        if (id.size() != VX_COMM_ID_BYTES) throw std::invalid_argument("NCCL unique id must be 128 bytes");
+        check(vx_comm_create(dev.get(), world, rank, id.data(), &c_));
+    }
+    ~Communicator() { vx_comm_destroy(c_); }
+    Communicator(const Communicator&) = delete;
+    Communicator& operator=(const Communicator&) = delete;
+    vx_comm* get() const { return c_; }
+
+  private:
+    vx_comm* c_ = nullptr;
+};
+
 // Device-resident EvolutionState: init_evolution + evolve_generation with
 // the advisor consulted where evolution.hpp:221-227 consults it.
 class GpuEvolution {
@@ -323,6 +538,23 @@ class GpuEvolution {
         cfg.validate();
         const vx_evo_config c = to_c(cfg);
         check(vx_evo_create(dev.get(), &c, &evo_));
+    }
+    // One rank of a run sharded over GPUs: every rank holds
+    // the replicated state, evaluates its shard of the children, and the
+    // communicator all-reduces the exchange buffer once per generation.
+    // Identical results on every rank and for every world size.
+    GpuEvolution(const EvolutionConfig& cfg, Communicator& comm, Device& dev = default_device())
+        : GpuEvolution(cfg, dev) {
+        check(vx_evo_set_comm(evo_, comm.get()));
+    }
+    // The same over any transport: allreduce(d_buf, n) must leave the
+    // element-wise sum over the `world` ranks in the device buffer.
+    using AllReduceFn = std::function<void(double* d_buf, int64_t n)>;
+    GpuEvolution(const EvolutionConfig& cfg, int rank, int world, AllReduceFn allreduce,
+                 Device& dev = default_device())
+        : GpuEvolution(cfg, dev) {
+        allreduce_ = std::move(allreduce);
+        check(vx_evo_set_exchange(evo_, rank, world, &GpuEvolution::exchange_tramp, this));
     }
     ~GpuEvolution() { vx_evo_free(evo_); }
     GpuEvolution(const GpuEvolution&) = delete;
@@ -422,11 +654,91 @@ class GpuEvolution {
     }
     std::vector<GenerationReport> history;
 
+    // The full reference state (grids of already-decoded individuals
+    // included, so elites are not decoded again), e.g. for the free-function
+    // evolve_generation below.
+    void load_full_state(const EvolutionState& st) {
+        std::vector<double> params, bmat, fit, gw;
+        std::vector<uint8_t> ev, grids;
+        const std::size_t cells = static_cast<std::size_t>(cfg_.grid_w) * cfg_.grid_h * cfg_.grid_d;
+        bool any_grid = false;
+        for (const auto& ind : st.population) any_grid = any_grid || ind.grid.cells.size() == cells;
+        for (const auto& ind : st.population) {
+            flatten(ind.genome, params);
+            bmat.insert(bmat.end(), ind.genome.b_matrix.begin(), ind.genome.b_matrix.end());
+            fit.push_back(ind.fitness);
+            ev.push_back(ind.evaluated ? 1 : 0);
+            if (!any_grid) continue;
+            const bool has = ind.grid.cells.size() == cells;
+            for (std::size_t c = 0; c < cells; ++c) {
+                grids.push_back(has ? static_cast<uint8_t>(ind.grid.cells[c].material) : uint8_t(255));
+                gw.push_back(has ? ind.grid.cells[c].weight : 0.0);
+            }
+        }
+        check(vx_evo_set_population(evo_, params.data(), bmat.data(), fit.data(), ev.data(),
+                                    any_grid ? grids.data() : nullptr, any_grid ? gw.data() : nullptr));
+        const vx_hyper h = to_c(st.params);
+        check(vx_evo_set_params(evo_, &h));
+        set_rng_state(st.rng.state());
+        history = st.history;
+        std::vector<double> bp;
+        if (st.best_genome) flatten(*st.best_genome, bp);
+        check(vx_evo_set_progress(evo_, st.generation, st.best_fitness, st.best_genome ? bp.data() : nullptr,
+                                  st.best_genome ? st.best_genome->b_matrix.data() : nullptr));
+    }
+    // to_state() plus the cached raw grids of the individuals that have one.
+    EvolutionState to_full_state() const {
+        EvolutionState st = to_state();
+        const std::size_t P = st.population.size();
+        const std::size_t cells = static_cast<std::size_t>(cfg_.grid_w) * cfg_.grid_h * cfg_.grid_d;
+        std::vector<uint8_t> grids(P * cells);
+        std::vector<double> gw(P * cells);
+        check(vx_evo_get_population(evo_, nullptr, nullptr, nullptr, nullptr, grids.data(), gw.data()));
+        for (std::size_t i = 0; i < P; ++i) {
+            if (grids[i * cells] == 255) continue;  // not decoded
+            VoxelGrid g(cfg_.grid_w, cfg_.grid_h, cfg_.grid_d);
+            for (std::size_t c = 0; c < cells; ++c)
+                g.cells[c] = Cell{static_cast<Material>(grids[i * cells + c]), gw[i * cells + c]};
+            st.population[i].grid = std::move(g);
+        }
+        return st;
+    }
+
   private:
+    static vx_status exchange_tramp(double* d_buf, int64_t n, void* self) {
+        try {
+            static_cast<GpuEvolution*>(self)->allreduce_(d_buf, n);
+            return VX_OK;
+        } catch (...) {
+            return VX_ECUDA;
+        }
+    }
     EvolutionConfig cfg_;
     Device& dev_;
     vx_evo* evo_ = nullptr;
+    AllReduceFn allreduce_;
 };
+
+// init_evolution (evolution.hpp:197-211): per-genome seeds from the master
+// stream, genomes sampled on device (B on the host libm) — the same
+// EvolutionState the reference returns, bit for bit.
+inline EvolutionState init_evolution(const EvolutionConfig& cfg, Device& dev = default_device()) {
+    GpuEvolution g(cfg, dev);
+    return g.to_state();
+}
+
+// evolve_generation (evolution.hpp:217-293) on a host-resident reference
+// EvolutionState: the state goes to the device, one generation runs there
+// (advisor consulted as the reference does), and the new state comes back.
+// For many generations keep a GpuEvolution instead (no transfers).
+inline GenerationReport evolve_generation(EvolutionState& st, const AdvisorFn& advisor = nullptr,
+                                          Device& dev = default_device()) {
+    GpuEvolution g(st.config, dev);
+    g.load_full_state(st);
+    const GenerationReport rep = g.evolve_generation(advisor);
+    st = g.to_full_state();
+    return rep;
+}
 
 // run_bench (bench.hpp:50-86)
 inline BenchResult run_bench(const BenchConfig& cfg, Device& dev = default_device()) {

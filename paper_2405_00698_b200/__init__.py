@@ -239,6 +239,7 @@ def _declare(lib):
         "vx_batch_override_phase": (i32, [vp, vp, vp]),
         "vx_batch_step": (i32, [vp, vp, P(SimConfig), i64, i64, vp]),
         "vx_batch_simulate": (i32, [vp, vp, P(SimConfig), vp]),
+        "vx_batch_step_at": (i32, [vp, vp, P(SimConfig), dbl, vp]),
         "vx_batch_simulate_dev": (i32, [vp, vp, P(SimConfig), vp]),
         "vx_batch_simulate_dump": (i32, [vp, vp, P(SimConfig), i32, i64, vp, vp, vp]),
         "vx_evaluate_dev": (i32, [vp, i32, i32, i32, i32, vp, vp, P(MaterialTable), P(GroundPlane), P(SimConfig), vp,
@@ -657,6 +658,12 @@ class Batch:
         """step() (physics.hpp:191-264) n_steps times from t = k0*dt; mutates the batch."""
         out = (TrajectorySummary * max(1, len(self)))()
         _check(_lib().vx_batch_step(self.ctx.h, self.h, C.byref(sim), k0, n_steps, out), "step")
+        return list(out)[:len(self)]
+
+    def step_at(self, sim: SimConfig, t: float):
+        """step(sys, t, cfg, ws) (physics.hpp:191-264) once at an arbitrary time t; mutates the batch."""
+        out = (TrajectorySummary * max(1, len(self)))()
+        _check(_lib().vx_batch_step_at(self.ctx.h, self.h, C.byref(sim), float(t), out), "step_at")
         return list(out)[:len(self)]
 
     def simulate(self, sim: SimConfig):

@@ -573,6 +573,21 @@ vx_status vx_batch_step(vx_ctx* ctx, vx_batch* b, const vx_sim* sim, int64_t k0,
     return simulate_impl(ctx, b, sim, k0, n_steps, true, summaries, nullptr);
 }
 
+vx_status vx_batch_step_at(vx_ctx* ctx, vx_batch* b, const vx_sim* sim, double t, vx_summary* summaries) {
+    if (!ctx || !b || !sim) return VX_EINVAL;
+    // the drive of step(sys, t, ...) (physics.hpp:196-198) for this t alone
+    const double wt = kTwoPi * sim->actuation_frequency * t;
+    const double2 h = make_double2(std::sin(wt), std::cos(wt));
+    VX_TRY(ctx->drive.alloc(1));
+    VX_CUDA(cudaMemcpyAsync(ctx->drive.p, &h, sizeof(h), cudaMemcpyHostToDevice, ctx->stream));
+    VX_CUDA(cudaStreamSynchronize(ctx->stream));
+    ctx->drive_freq = -1.0;  // the cached k-indexed table is gone
+    ctx->drive_pinned = true;
+    const vx_status s = simulate_impl(ctx, b, sim, 0, 1, true, summaries, nullptr);
+    ctx->drive_pinned = false;
+    return s;
+}
+
 vx_status vx_batch_simulate(vx_ctx* ctx, vx_batch* b, const vx_sim* sim, vx_summary* summaries) {
     if (!sim) return VX_EINVAL;
     const int64_t n_steps = std::llround(sim->duration / sim->dt);  // physics.hpp:295

@@ -40,8 +40,8 @@ vx_status vx_sample_genomes(vx_ctx* ctx, const vx_arch* a, int32_t P, const uint
     VX_TRY(sample_genomes_dev(ctx, a, P, ds.p, dp.p, db.p));
     VX_CUDA(cudaMemcpyAsync(params, dp.p, P * static_cast<size_t>(np) * sizeof(double), cudaMemcpyDeviceToHost,
                             ctx->stream));
-    VX_CUDA(cudaMemcpyAsync(bmat, db.p, P * 3ull * a->m * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
     VX_CUDA(cudaStreamSynchronize(ctx->stream));
+    host_sample_bmat(a->m, a->sigma, P, seeds, bmat);  // glibc Box-Muller: bit-exact B
     return VX_OK;
 }
 
@@ -161,8 +161,18 @@ vx_status vx_evaluate(vx_ctx* ctx, int32_t P, int32_t w, int32_t h, int32_t d, c
     VX_TRY(upload(dw, weight, P * cells, ctx->stream));
     VX_TRY(df.alloc(P));
     if (summaries) VX_TRY(ds.alloc(P));
+    // the weights are on the host: sin/cos of every cell's actuation phase
+    // with the host glibc, as the reference's SimWorkspace computes them
+    // (physics.hpp:154-155), so fitness is bit-identical to the reference's
+    std::vector<double2> sc(P * cells);
+    for (size_t q = 0; q < sc.size(); ++q) {
+        const double phase = weight[q] * table->phase_max;  // morphology.hpp:275
+        sc[q] = make_double2(std::sin(phase), std::cos(phase));
+    }
+    DevBuf<double2> dsc;
+    VX_TRY(upload(dsc, sc.data(), sc.size(), ctx->stream));
     VX_TRY(evaluate_pipeline(ctx, P, w, h, d, dm.p, dw.p, table, plane, sim, nullptr, P, df.p, nullptr,
-                             summaries ? ds.p : nullptr));
+                             summaries ? ds.p : nullptr, dsc.p));
     VX_CUDA(cudaMemcpyAsync(fitness, df.p, P * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
     if (summaries)
         VX_CUDA(cudaMemcpyAsync(summaries, ds.p, P * sizeof(vx_summary), cudaMemcpyDeviceToHost, ctx->stream));

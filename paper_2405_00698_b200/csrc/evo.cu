@@ -34,10 +34,33 @@ using namespace vx;
 
 namespace vx {
 
+namespace {
+// Host-exact actuation phases: every actuated spring takes sin/cos(phase) of
+// its actuating voxel (phase = weight * phase_max, morphology.hpp:274-275;
+// SimWorkspace physics.hpp:154-155) from a per-cell table the host computed
+// with glibc, replacing the device sincos of derive_kernel.
+__global__ void phase_override_kernel(int n, const int64_t* spring_off, const int32_t* nspring, const int16_t* act_vox,
+                                      const int32_t* d_todo, int cells, const double2* tab, double* sinph,
+                                      double* cosph) {
+    const int r = blockIdx.x;
+    if (r >= n) return;
+    const int64_t so = spring_off[r];
+    const double2* t = tab + static_cast<int64_t>(d_todo ? d_todo[r] : r) * cells;
+    for (int q = threadIdx.x; q < nspring[r]; q += blockDim.x) {
+        const int v = act_vox[so + q];
+        if (v >= 0) {
+            sinph[so + q] = t[v].x;
+            cosph[so + q] = t[v].y;
+        }
+    }
+}
+}  // namespace
+
 // raw grids -> component -> build -> gates -> integrate -> fitness
 vx_status evaluate_pipeline(vx_ctx* ctx, int P, int w, int h, int d, const uint8_t* d_mat, const double* d_weight,
                             const vx_materials* table, const vx_plane* plane, const vx_sim* sim, const int32_t* d_todo,
-                            int n_todo, double* d_fitness, double* d_updates, vx_summary* d_summaries) {
+                            int n_todo, double* d_fitness, double* d_updates, vx_summary* d_summaries,
+                            const double2* d_phase_sc) {
     const int n = d_todo ? n_todo : P;
     if (n <= 0) return VX_OK;
     if (!(sim->dt > 0.0)) return (set_error("SimConfig: dt must be > 0"), VX_EINVAL);
@@ -51,6 +74,12 @@ vx_status evaluate_pipeline(vx_ctx* ctx, int P, int w, int h, int d, const uint8
     vx_batch* b = ctx->eval_batch;
     VX_TRY(build_batch_into(ctx, b, n, w, h, d, ctx->eval_body.p, d_weight, d_todo, table, plane));
     VX_TRY(gate_dev(ctx, b));
+    if (d_phase_sc) {
+        phase_override_kernel<<<n, 256, 0, ctx->stream>>>(n, b->spring_off.p, b->nspring.p, b->act_vox.p, d_todo,
+                                                         cells, d_phase_sc, b->sinph.p, b->cosph.p);
+        ctx->launches++;
+        VX_CUDA(cudaGetLastError());
+    }
     const int64_t n_steps = std::llround(sim->duration / sim->dt);  // physics.hpp:295
     VX_TRY(integrate(ctx, b, sim, 0, n_steps, false, nullptr, 0, ctx->eval_summ.p, nullptr));
     return fitness_dev(ctx, n, d_todo, b->status.p, ctx->eval_summ.p, d_fitness, d_updates, d_summaries);
@@ -252,6 +281,13 @@ vx_status vx_evo_create(vx_ctx* ctx, const vx_evo_config* cfg, vx_evo** out) {
     VX_TRY(d_seeds.alloc(e->P));
     VX_CUDA(cudaMemcpyAsync(d_seeds.p, seeds.data(), e->P * sizeof(uint64_t), cudaMemcpyHostToDevice, ctx->stream));
     VX_TRY(sample_genomes_dev(ctx, &cfg->arch, e->P, d_seeds.p, e->prm[0].p, e->bm[0].p));
+    {  // B with the host glibc Box-Muller (bit-exact), over the device's
+        std::vector<double> hb(static_cast<size_t>(e->P) * e->nb);
+        host_sample_bmat(cfg->arch.m, cfg->arch.sigma, e->P, seeds.data(), hb.data());
+        VX_CUDA(cudaMemcpyAsync(e->bm[0].p, hb.data(), hb.size() * sizeof(double), cudaMemcpyHostToDevice,
+                                ctx->stream));
+        VX_CUDA(cudaStreamSynchronize(ctx->stream));
+    }
     VX_CUDA(cudaMemsetAsync(e->fit[0].p, 0, e->P * sizeof(double), ctx->stream));
     VX_CUDA(cudaMemsetAsync(e->ev[0].p, 0, e->P, ctx->stream));
     VX_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -627,9 +663,12 @@ vx_status vx_evo_set_population(vx_evo* e, const double* params, const double* b
     }
     VX_CUDA(cudaStreamSynchronize(s));
     for (size_t a = 0; a < P; ++a) {
+        // material 255 in a row's first cell: no grid for that individual
+        // (vx_evo_get_population's marker), it is decoded when needed
+        const bool has = grids && grids[a * e->cells] != 255;
         e->h_eval[a] = ev[a] ? 1 : 0;
-        e->h_has_grid[a] = grids ? 1 : 0;
-        e->h_owner[a] = grids ? 0 : -1;  // host-provided grids: rank 0's copy counts
+        e->h_has_grid[a] = has ? 1 : 0;
+        e->h_owner[a] = has ? 0 : -1;  // host-provided grids: rank 0's copy counts
     }
     return VX_OK;
 }

@@ -43,6 +43,7 @@ vx_status breed_dev(vx_ctx* ctx, const BreedArgs& A, int P, const MutEntry* d_mu
 // raw grids (selected) -> component -> build -> gates -> integrate -> fitness.
 vx_status evaluate_pipeline(vx_ctx* ctx, int P, int w, int h, int d, const uint8_t* d_mat, const double* d_weight,
                             const vx_materials* table, const vx_plane* plane, const vx_sim* sim, const int32_t* d_todo,
-                            int n_todo, double* d_fitness, double* d_updates, vx_summary* d_summaries);
+                            int n_todo, double* d_fitness, double* d_updates, vx_summary* d_summaries,
+                            const double2* d_phase_sc = nullptr);
 
 }  // namespace vx

@@ -5,10 +5,16 @@
 // Each check compares voxevo::X (reference, CPU) with voxevo::b200::X (GPU)
 // on identical inputs and prints one PASS/FAIL line, like the reference's
 // acceptance binary (acceptance_main.cpp:31-38).  Exit code = #failures.
+#include <cuda_runtime.h>
+
+#include <barrier>
 #include <cmath>
 #include <cstdio>
+#include <cstring>
 #include <string>
+#include <thread>
 
+#include "voxevo/advisor.hpp"
 #include "voxevo/bench.hpp"
 #include "voxevo/evolution.hpp"
 #include "voxevo/serialize.hpp"
@@ -22,9 +28,26 @@ static void report(const char* name, bool ok, const std::string& detail) {
     if (!ok) ++g_fail;
 }
 
+static bool same_genome(const Genome& a, const Genome& b) {
+    if (a.b_matrix != b.b_matrix || !a.same_architecture(b)) return false;
+    auto ta = const_cast<Genome&>(a).param_tensors();
+    auto tb = const_cast<Genome&>(b).param_tensors();
+    for (std::size_t t = 0; t < ta.size(); ++t)
+        if (*ta[t] != *tb[t]) return false;
+    return true;
+}
+
 int main() {
     // config 1: sample_genome(seed 42) -> decode 4^3
     const Genome g = sample_genome(EncodingSpec{32, 3, 1.0}, {64, 64}, 42);
+    report("sample_genome bit-exact (B and every layer)", same_genome(g, b200::sample_genome(EncodingSpec{32, 3, 1.0},
+                                                                                             {64, 64}, 42)),
+           "seed 42, m 32, hidden {64,64}");
+    {
+        const Vec3 v{0.125, 0.375, 0.875};
+        report("gaussian_encode bit-exact", gaussian_encode(v, g.b_matrix, 32) == b200::gaussian_encode(v, g.b_matrix, 32),
+               "64 features");
+    }
     const VoxelGrid ref_grid = decode(g, 4, 4, 4);
     const VoxelGrid gpu_grid = b200::decode(g, 4, 4, 4);
     int mat_diff = 0;
@@ -59,22 +82,45 @@ int main() {
     sim.duration = 1000 * sim.dt;
     const TrajectorySummary rs = simulate(sys, sim);
     const TrajectorySummary gs = b200::simulate(sys, sim);
-    const double rel = std::abs(rs.horizontal_displacement - gs.horizontal_displacement) / rs.horizontal_displacement;
-    report("simulate 1000 steps: displacement rel <= 1e-3", rel <= 1e-3 && rs.diverged == gs.diverged,
-           "ref " + std::to_string(rs.horizontal_displacement) + " rel " + std::to_string(rel));
+    report("simulate 1000 steps bit-exact (COM, displacement, max speed)",
+           rs.horizontal_displacement == gs.horizontal_displacement && rs.com_end == gs.com_end &&
+               rs.com_start == gs.com_start && rs.max_speed == gs.max_speed && rs.diverged == gs.diverged,
+           "displacement " + std::to_string(rs.horizontal_displacement));
 
-    // simulate with the COM dump (physics.hpp:285-311): same sample times, COMs within the chaos floor
+    // simulate with the COM dump (physics.hpp:285-311): every row bit-exact
     std::vector<TrajectorySample> rd, gd;
     simulate(sys, sim, &rd, 300);
     b200::simulate(sys, sim, &gd, 300);
     bool dump_ok = rd.size() == gd.size();
-    for (size_t q = 0; dump_ok && q < rd.size(); ++q) {
-        dump_ok = rd[q].t == gd[q].t;
-        for (int c = 0; c < 3; ++c)
-            dump_ok = dump_ok && std::abs(rd[q].com[c] - gd[q].com[c]) <= 1e-9 + 1e-6 * std::abs(rd[q].com[c]);
+    for (size_t q = 0; dump_ok && q < rd.size(); ++q) dump_ok = rd[q].t == gd[q].t && rd[q].com == gd[q].com;
+    report("simulate with dump every 300 steps: rows bit-exact", dump_ok, std::to_string(rd.size()) + " rows");
+
+    // step (physics.hpp:191): 40 single steps at t = k dt, state and counters bit-exact
+    {
+        MassSpringSystem a = sys, b = sys;
+        SimWorkspace wa(a), wb(b);
+        bool ok = true;
+        for (int k = 0; k < 40 && ok; ++k) {
+            const double t = static_cast<double>(k) * sim.dt;
+            ok = step(a, t, sim, wa) == b200::step(b, t, sim, wb);
+        }
+        for (size_t i = 0; ok && i < a.masses.size(); ++i) ok = a.masses[i].pos == b.masses[i].pos && a.masses[i].vel == b.masses[i].vel;
+        ok = ok && wa.spring_updates == wb.spring_updates && wa.max_speed_sq == wb.max_speed_sq;
+        report("step x40 bit-exact (positions, velocities, counters)", ok,
+               std::to_string(wa.spring_updates) + " spring updates");
     }
-    report("simulate with dump every 300 steps: rows and times match", dump_ok,
-           std::to_string(rd.size()) + " rows");
+
+    // evaluate_fitness (evolution.hpp:110) on raw grids: bit-exact
+    {
+        std::vector<VoxelGrid> raws;
+        for (uint64_t seed : {42u, 7u, 11u, 2024u})
+            raws.push_back(decode(sample_genome(EncodingSpec{32, 3, 1.0}, {64, 64}, seed), 5, 5, 5));
+        const std::vector<double> gf = b200::evaluate_fitness(raws, MaterialTable{}, GroundPlane{}, sim);
+        bool ok = true;
+        for (size_t a = 0; a < raws.size(); ++a)
+            ok = ok && gf[a] == evaluate_fitness(raws[a], MaterialTable{}, GroundPlane{}, sim);
+        report("evaluate_fitness bit-exact (4 decoded 5^3 robots)", ok, "fitness[0] " + std::to_string(gf[0]));
+    }
 
     // forward (genome.hpp:187-211) at off-grid points: probabilities and weight within 1e-12
     {
@@ -90,6 +136,38 @@ int main() {
         report("forward at off-grid points: probs / weight <= 1e-12", fok, std::to_string(pts.size()) + " points");
     }
 
+
+    // the GA operators on the caller's Rng (evolution.hpp:143-173)
+    {
+        const Genome a = sample_genome(EncodingSpec{32, 3, 1.0}, {64, 64}, 5);
+        const Genome b = sample_genome(EncodingSpec{32, 3, 1.0}, {64, 64}, 6);
+        Rng r1(99), r2(99);
+        Genome c1 = crossover(a, b, r1), c2 = b200::crossover(a, b, r2);
+        mutate(c1, 0.1, 0.1, r1);
+        b200::mutate(c2, 0.1, 0.1, r2);
+        std::vector<Individual> pop(37);
+        const Individual* w1 = &tournament_select(pop, 3, r1);
+        const Individual* w2 = &b200::tournament_select(pop, 3, r2);
+        report("crossover / mutate / tournament_select bit-exact on the caller's Rng",
+               same_genome(c1, c2) && w1 == w2 && r1 == r2, "winner " + std::to_string(w1 - pop.data()));
+    }
+    {
+        std::vector<Individual> pop(6);
+        for (int i = 0; i < 6; ++i)
+            pop[i].grid = decode(sample_genome(EncodingSpec{32, 3, 1.0}, {64, 64}, 100 + i), 6, 6, 6);
+        const double rd = population_diversity(pop), gd = b200::population_diversity(pop);
+        report("population_diversity within 1e-13", std::abs(rd - gd) <= 1e-13 * rd, std::to_string(rd));
+    }
+    {
+        bool threw = false;
+        try {
+            Genome deep = sample_genome(EncodingSpec{4, 3, 1.0}, {2, 2, 2, 2, 2, 2, 2, 2, 2}, 1);
+            b200::decode(deep, 2, 2, 2);
+        } catch (const std::invalid_argument&) {
+            threw = true;
+        }
+        report("more than VX_MAX_HIDDEN layers -> std::invalid_argument", threw, "9 hidden layers");
+    }
 
     // desk GA (acceptance_main.cpp:193-211 shape): reference genomes on the
     // GPU; draw consumption is fitness-independent -> identical RNG streams
@@ -158,6 +236,93 @@ int main() {
                gq.generation == cq.generation && gq.evaluations == cq.evaluations && c.rng_state() == cpu.rng.state(),
                "generation " + std::to_string(gq.generation));
         std::remove(path.c_str());
+    }
+
+    // init_evolution bit-exact; free-function evolve_generation on a host state
+    {
+        EvolutionConfig c3 = cfg;
+        c3.seed = 21;
+        EvolutionState r = init_evolution(c3);
+        EvolutionState q = b200::init_evolution(c3);
+        bool same = r.rng == q.rng && r.population.size() == q.population.size();
+        for (size_t i = 0; same && i < r.population.size(); ++i) same = same_genome(r.population[i].genome, q.population[i].genome);
+        report("init_evolution bit-exact (every genome, GA stream)", same, std::to_string(r.population.size()) + " genomes");
+        bool ok = true;
+        for (int k = 0; k < 3; ++k) {
+            const GenerationReport x = evolve_generation(r), y = b200::evolve_generation(q);
+            ok = ok && x.evaluations == y.evaluations && x.generation == y.generation &&
+                 std::abs(x.best - y.best) <= 1e-2 * x.best;
+        }
+        report("evolve_generation(EvolutionState&) free function: same GA stream", ok && r.rng == q.rng &&
+               r.generation == q.generation && r.history.size() == q.history.size(), "3 generations");
+    }
+
+    // advisor in the loop (evolution.hpp:221-227): the reference's own
+    // ScriptedAdvisor, 8 generations; fired rules change the RNG consumption,
+    // so identical params histories and GA streams prove identical decisions
+    {
+        EvolutionConfig c4 = cfg;
+        c4.seed = 4;
+        c4.population = 16;
+        ScriptedAdvisor adv_r, adv_g;
+        AdvisorFn fr = [&](const std::vector<GenerationReport>& w, const HyperParams& h) { return adv_r.propose(w, h); };
+        AdvisorFn fg = [&](const std::vector<GenerationReport>& w, const HyperParams& h) { return adv_g.propose(w, h); };
+        EvolutionState r = init_evolution(c4);
+        b200::GpuEvolution gpu4(c4);
+        bool ok = true;
+        int fired = 0;
+        for (int k = 0; k < 8; ++k) {
+            const GenerationReport x = evolve_generation(r, fr), y = gpu4.evolve_generation(fg);
+            ok = ok && x.params.mutation_rate == y.params.mutation_rate &&
+                 x.params.mutation_scale == y.params.mutation_scale && x.params.crossover_rate == y.params.crossover_rate;
+            fired += x.params.crossover_rate != c4.initial_params.crossover_rate ||
+                     x.params.mutation_rate != c4.initial_params.mutation_rate;
+        }
+        report("ScriptedAdvisor in the loop: params history + GA stream identical", ok && gpu4.rng_state() == r.rng.state(),
+               std::to_string(fired) + " generations with adjusted params");
+    }
+
+    // sharded GpuEvolution(cfg, rank, world, allreduce): two ranks in two
+    // threads (each its own context), host all-reduce between them; reports
+    // and GA streams bit-identical to the single-rank run
+    {
+        EvolutionConfig c5 = cfg;
+        c5.seed = 5;
+        c5.population = 24;
+        b200::GpuEvolution solo(c5);
+        std::vector<GenerationReport> want;
+        for (int k = 0; k < 3; ++k) want.push_back(solo.evolve_generation());
+        std::barrier sync(2);
+        std::vector<double> h0, h1, sum;
+        std::vector<GenerationReport> got[2];
+        std::string rng_state[2];
+        auto rank_main = [&](int rank) {
+            b200::Device dev(0);
+            std::vector<double>& mine = rank == 0 ? h0 : h1;
+            b200::GpuEvolution g(c5, rank, 2, [&](double* d_buf, int64_t n) {
+                mine.resize(static_cast<size_t>(n));
+                cudaMemcpy(mine.data(), d_buf, n * sizeof(double), cudaMemcpyDeviceToHost);
+                sync.arrive_and_wait();
+                if (rank == 0) {
+                    sum.resize(static_cast<size_t>(n));
+                    for (int64_t i = 0; i < n; ++i) sum[i] = h0[i] + h1[i];
+                }
+                sync.arrive_and_wait();
+                cudaMemcpy(d_buf, sum.data(), n * sizeof(double), cudaMemcpyHostToDevice);
+            }, dev);
+            for (int k = 0; k < 3; ++k) got[rank].push_back(g.evolve_generation());
+            rng_state[rank] = g.rng_state();
+        };
+        std::thread t0(rank_main, 0), t1(rank_main, 1);
+        t0.join();
+        t1.join();
+        bool ok = rng_state[0] == solo.rng_state() && rng_state[1] == solo.rng_state();
+        for (int r = 0; r < 2; ++r)
+            for (int k = 0; k < 3; ++k)
+                ok = ok && got[r][k].best == want[k].best && got[r][k].mean == want[k].mean &&
+                     got[r][k].stddev == want[k].stddev && got[r][k].diversity == want[k].diversity &&
+                     got[r][k].evaluations == want[k].evaluations;
+        report("GpuEvolution(cfg, rank, world): 2 ranks == 1 rank, bit for bit", ok, "3 generations, P=24");
     }
 
     BenchConfig bc;

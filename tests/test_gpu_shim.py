@@ -17,4 +17,4 @@ def test_cpp_shim_drop_in():
     out = subprocess.run([DEMO], capture_output=True, text=True, timeout=600)
     print(out.stdout)
     assert out.returncode == 0, out.stdout + out.stderr
-    assert out.stdout.count("PASS") == 11 and "FAIL" not in out.stdout
+    assert "FAIL" not in out.stdout and out.stdout.count("PASS") >= 22, out.stdout
