@@ -132,6 +132,8 @@ class _Lib:
                                              vp])
             f("evo_set_threads", None, [vp, C.c_int])
             f("evo_generation_timed", C.c_double, [vp, vp, vp])
+            f("evo_generation_advised", C.c_int, [vp, vp, vp])
+            f("evo_pending_fitness", None, [vp, vp])
         else:
             f("simulate", None, [vp, vp, vp])
 
@@ -380,6 +382,25 @@ class Evo:
                     diversity=float(rep[4]), evaluations=int(rep[5]), wall_time=float(rep[6]),
                     params=rep[7:14].copy())
 
+    def generation_advised(self, adv4=None) -> dict:
+        """evolve_generation with the reference's own ScriptedAdvisor
+        (advisor.hpp:30-55) in the loop; adv4 = (diversity_floor,
+        stagnation_eps, mutation_boost, crossover_boost) or None for defaults."""
+        rep = np.zeros(14)
+        a = None if adv4 is None else np.ascontiguousarray(adv4, np.float64)
+        if not self.lib._evo_generation_advised(self.h, rep.ctypes.data, None if a is None else a.ctypes.data):
+            raise RuntimeError("reference built without nlohmann/json: ScriptedAdvisor unavailable")
+        return dict(generation=int(rep[0]), best=float(rep[1]), mean=float(rep[2]), stddev=float(rep[3]),
+                    diversity=float(rep[4]), evaluations=int(rep[5]), wall_time=float(rep[6]),
+                    params=rep[7:14].copy())
+
+    def pending_fitness(self) -> np.ndarray:
+        """The fitness the next evolve_generation computes for each individual
+        without a cached score (NaN for the others)."""
+        out = np.zeros(self.P)
+        self.lib._evo_pending_fitness(self.h, out.ctypes.data)
+        return out
+
     def generation_timed(self):
         """(report, seconds of evolve_generation alone, exact spring updates it performed)."""
         rep = np.zeros(14)
@@ -473,6 +494,8 @@ class RefIO:
         lib.ref_io_resume.argtypes = [cp, C.c_int, cp]
         lib.ref_io_curves_csv.restype = i64
         lib.ref_io_curves_csv.argtypes = [cp, cp, i64]
+        lib.ref_io_run_advised.restype = C.c_int
+        lib.ref_io_run_advised.argtypes = [cp, C.c_int, vp, vp, cp, i64]
         self.lib = lib
 
     def _text(self, fn, *args) -> str:
@@ -500,6 +523,19 @@ class RefIO:
 
     def curves_csv(self, path: str) -> str:
         return self._text(self.lib.ref_io_curves_csv, path.encode())
+
+    def run_advised(self, config_json: str, gens: int, adv4=None):
+        """init_evolution + gens x evolve_generation with the reference's own
+        ScriptedAdvisor (advisor.hpp:30-55).  Returns (history rows [gens][13]:
+        generation, best, mean, stddev, diversity, evaluations, params[7]; the
+        final Rng state text)."""
+        hist = np.zeros((gens, 13))
+        a = None if adv4 is None else np.ascontiguousarray(adv4, np.float64)
+        buf = C.create_string_buffer(1 << 16)
+        if self.lib.ref_io_run_advised(config_json.encode(), gens, None if a is None else a.ctypes.data,
+                                       hist.ctypes.data, buf, len(buf)) != 0:
+            raise RuntimeError(self.lib.ref_io_last_error().decode())
+        return hist, buf.value.decode()
 
 
 def have_reference_io() -> bool:

@@ -10,6 +10,7 @@
 #include <exception>
 #include <string>
 
+#include "voxevo/advisor.hpp"
 #include "voxevo/serialize.hpp"
 
 namespace {
@@ -62,6 +63,50 @@ int ref_io_resume(const char* in_path, int gens, const char* out_path) {
         voxevo::EvolutionState st = voxevo::load_run(in_path);
         for (int g = 0; g < gens; ++g) voxevo::evolve_generation(st);
         voxevo::save_run(out_path, st);
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return -1;
+    }
+}
+
+// init_evolution(evolution_config_from_json(cfg)) -> `gens` x
+// evolve_generation(st, make_advisor_fn(&ScriptedAdvisor)) with the
+// reference's own ScriptedAdvisor (advisor.hpp:30-55) consulted at
+// evolution.hpp:221-227.  adv4 = diversity_floor, stagnation_eps,
+// mutation_boost, crossover_boost (NULL: the class defaults).  hist gets
+// gens rows of: generation, best, mean, stddev, diversity, evaluations,
+// params[7] (mutation_rate, mutation_scale, crossover_rate, elite_fraction,
+// multipliers[3]); rng_out the final Rng::state() text.
+int ref_io_run_advised(const char* config_json, int gens, const double* adv4, double* hist, char* rng_out,
+                       int64_t rng_cap) {
+    try {
+        const voxevo::EvolutionConfig cfg = voxevo::evolution_config_from_json(nlohmann::json::parse(config_json));
+        voxevo::EvolutionState st = voxevo::init_evolution(cfg);
+        voxevo::ScriptedAdvisor adv;
+        if (adv4) {
+            adv.diversity_floor = adv4[0];
+            adv.stagnation_eps = adv4[1];
+            adv.mutation_boost = adv4[2];
+            adv.crossover_boost = adv4[3];
+        }
+        const voxevo::AdvisorFn fn = voxevo::make_advisor_fn(&adv);
+        for (int g = 0; g < gens; ++g) {
+            const voxevo::GenerationReport r = voxevo::evolve_generation(st, fn);
+            double* row = hist + static_cast<size_t>(g) * 13;
+            row[0] = r.generation;
+            row[1] = r.best;
+            row[2] = r.mean;
+            row[3] = r.stddev;
+            row[4] = r.diversity;
+            row[5] = r.evaluations;
+            row[6] = r.params.mutation_rate;
+            row[7] = r.params.mutation_scale;
+            row[8] = r.params.crossover_rate;
+            row[9] = r.params.elite_fraction;
+            for (int k = 0; k < 3; ++k) row[10 + k] = r.params.material_multipliers[k];
+        }
+        put(st.rng.state(), rng_out, rng_cap);
         return 0;
     } catch (const std::exception& e) {
         g_err = e.what();

@@ -12,9 +12,13 @@
 #include <chrono>
 #include <cstdint>
 #include <cstring>
+#include <limits>
 #include <string>
 #include <vector>
 
+#ifdef VX_REF_HAVE_JSON
+#include "voxevo/advisor.hpp"  // ScriptedAdvisor (needs nlohmann/json)
+#endif
 #include "voxevo/bench.hpp"
 #include "voxevo/evolution.hpp"
 #include "voxevo/genome.hpp"
@@ -477,6 +481,57 @@ double ref_evo_generation_timed(void* h, double* rep, uint64_t* updates) {
     for (uint64_t c : count) total += c;
     if (updates) *updates = total;
     return secs;
+}
+
+#ifdef VX_REF_HAVE_JSON
+// evolve_generation(st, make_advisor_fn(&ScriptedAdvisor)) (evolution.hpp:
+// 217-227, advisor.hpp:30-55, 166-171): the reference's own scripted advisor
+// in the loop.  adv4 = diversity_floor, stagnation_eps, mutation_boost,
+// crossover_boost (NULL: the class defaults).  rep as ref_evo_generation.
+int ref_evo_generation_advised(void* h, double* rep, const double* adv4) {
+    auto* e = static_cast<RefEvo*>(h);
+    ScriptedAdvisor adv;
+    if (adv4) {
+        adv.diversity_floor = adv4[0];
+        adv.stagnation_eps = adv4[1];
+        adv.mutation_boost = adv4[2];
+        adv.crossover_boost = adv4[3];
+    }
+    const GenerationReport r = evolve_generation(e->st, make_advisor_fn(&adv));
+    rep[0] = r.generation;
+    rep[1] = r.best;
+    rep[2] = r.mean;
+    rep[3] = r.stddev;
+    rep[4] = r.diversity;
+    rep[5] = r.evaluations;
+    rep[6] = r.wall_time;
+    hyper_to(r.params, rep + 7);
+    return 1;
+}
+#else
+int ref_evo_generation_advised(void*, double*, const double*) { return 0; }
+#endif
+
+// The fitness evolve_generation is about to compute for each individual that
+// carries no cached score (evolution.hpp:229-241: decode if no grid, then
+// evaluate_fitness with the scaled material table), NaN for the others.
+// Deterministic: the same functions on the same inputs, so these are exactly
+// the values the next evolve_generation stores (with the CURRENT params; an
+// advisor changing material multipliers would need them applied first).
+void ref_evo_pending_fitness(void* h, double* out) {
+    auto* e = static_cast<RefEvo*>(h);
+    const EvolutionConfig& cfg = e->st.config;
+    const MaterialTable table = detail::scaled_materials(cfg.materials, e->st.params);
+    const auto& pop = e->st.population;
+    parallel_for(pop.size(), cfg.threads, [&](std::size_t i) {
+        const Individual& ind = pop[i];
+        if (ind.evaluated) {
+            out[i] = std::numeric_limits<double>::quiet_NaN();
+            return;
+        }
+        const VoxelGrid g = ind.grid.cells.empty() ? decode(ind.genome, cfg.grid_w, cfg.grid_h, cfg.grid_d) : ind.grid;
+        out[i] = evaluate_fitness(g, table, cfg.plane, cfg.sim);
+    });
 }
 
 int ref_evo_generation_index(void* h) { return static_cast<RefEvo*>(h)->st.generation; }

@@ -239,47 +239,84 @@ int main() {
     }
 
     // init_evolution bit-exact; free-function evolve_generation on a host state
+    // (the reference's default step, dt 1e-5 x 5000: fitness within rtol 1e-3;
+    // the GA stream's consumption is fitness-independent without an advisor)
     {
         EvolutionConfig c3 = cfg;
         c3.seed = 21;
+        c3.sim = SimConfig{};
         EvolutionState r = init_evolution(c3);
         EvolutionState q = b200::init_evolution(c3);
         bool same = r.rng == q.rng && r.population.size() == q.population.size();
         for (size_t i = 0; same && i < r.population.size(); ++i) same = same_genome(r.population[i].genome, q.population[i].genome);
         report("init_evolution bit-exact (every genome, GA stream)", same, std::to_string(r.population.size()) + " genomes");
         bool ok = true;
+        double rel0 = 0.0;
         for (int k = 0; k < 3; ++k) {
             const GenerationReport x = evolve_generation(r), y = b200::evolve_generation(q);
-            ok = ok && x.evaluations == y.evaluations && x.generation == y.generation &&
-                 std::abs(x.best - y.best) <= 1e-2 * x.best;
+            ok = ok && x.evaluations == y.evaluations && x.generation == y.generation;
+            if (k == 0) rel0 = std::abs(x.best - y.best) / x.best;
         }
-        report("evolve_generation(EvolutionState&) free function: same GA stream", ok && r.rng == q.rng &&
-               r.generation == q.generation && r.history.size() == q.history.size(), "3 generations");
+        report("evolve_generation(EvolutionState&) free function: same GA stream",
+               ok && rel0 <= 1e-3 && r.rng == q.rng && r.generation == q.generation && r.history.size() == q.history.size(),
+               "3 generations, gen-0 best rel " + std::to_string(rel0));
     }
 
     // advisor in the loop (evolution.hpp:221-227): the reference's own
-    // ScriptedAdvisor, 8 generations; fired rules change the RNG consumption,
-    // so identical params histories and GA streams prove identical decisions
+    // ScriptedAdvisor on both sides, 10 generations.  Lock-step with teacher
+    // forcing at the exchange point (world 1): the device evaluates every
+    // pending robot (checked within 5e-2, the dt = 1e-4 chaos floor), then the
+    // reference's fitness replaces it, so one chaotic near-tie cannot send the
+    // runs apart; fired rules change the RNG consumption, so identical params
+    // histories, reports, populations and GA streams prove identical decisions.
     {
         EvolutionConfig c4 = cfg;
         c4.seed = 4;
         c4.population = 16;
+        c4.grid_w = c4.grid_h = c4.grid_d = 4;
+        c4.sim.duration = 0.1;
         ScriptedAdvisor adv_r, adv_g;
-        AdvisorFn fr = [&](const std::vector<GenerationReport>& w, const HyperParams& h) { return adv_r.propose(w, h); };
-        AdvisorFn fg = [&](const std::vector<GenerationReport>& w, const HyperParams& h) { return adv_g.propose(w, h); };
+        const AdvisorFn fr = make_advisor_fn(&adv_r), fg = make_advisor_fn(&adv_g);
         EvolutionState r = init_evolution(c4);
-        b200::GpuEvolution gpu4(c4);
+        std::vector<double> forced;
+        double worst = 0.0;
+        b200::GpuEvolution gpu4(c4, 0, 1, [&](double* d_buf, int64_t n) {
+            std::vector<double> h(static_cast<size_t>(n));
+            cudaMemcpy(h.data(), d_buf, n * sizeof(double), cudaMemcpyDeviceToHost);
+            for (size_t i = 0; i < forced.size(); ++i)
+                if (!std::isnan(forced[i])) {
+                    worst = std::max(worst, std::abs(h[i] - forced[i]) / std::max(std::abs(forced[i]), 1e-12));
+                    h[i] = forced[i];
+                }
+            cudaMemcpy(d_buf, h.data(), n * sizeof(double), cudaMemcpyHostToDevice);
+        });
+        gpu4.set_population(r.population);
+        gpu4.set_rng_state(r.rng.state());
         bool ok = true;
         int fired = 0;
-        for (int k = 0; k < 8; ++k) {
-            const GenerationReport x = evolve_generation(r, fr), y = gpu4.evolve_generation(fg);
-            ok = ok && x.params.mutation_rate == y.params.mutation_rate &&
-                 x.params.mutation_scale == y.params.mutation_scale && x.params.crossover_rate == y.params.crossover_rate;
-            fired += x.params.crossover_rate != c4.initial_params.crossover_rate ||
-                     x.params.mutation_rate != c4.initial_params.mutation_rate;
+        for (int k = 0; k < 10; ++k) {
+            const MaterialTable table = detail::scaled_materials(c4.materials, r.params);
+            forced.assign(r.population.size(), std::nan(""));
+            for (size_t i = 0; i < r.population.size(); ++i)
+                if (!r.population[i].evaluated)
+                    forced[i] = evaluate_fitness(decode(r.population[i].genome, c4.grid_w, c4.grid_h, c4.grid_d), table,
+                                                 c4.plane, c4.sim);
+            const GenerationReport y = gpu4.evolve_generation(fg), x = evolve_generation(r, fr);
+            ok = ok && x.params == y.params && x.best == y.best && x.mean == y.mean && x.stddev == y.stddev &&
+                 x.evaluations == y.evaluations && std::abs(x.diversity - y.diversity) <= 1e-13 * x.diversity &&
+                 (x.diversity < adv_r.diversity_floor) == (y.diversity < adv_g.diversity_floor);
+            fired += !(x.params == c4.initial_params);
         }
-        report("ScriptedAdvisor in the loop: params history + GA stream identical", ok && gpu4.rng_state() == r.rng.state(),
-               std::to_string(fired) + " generations with adjusted params");
+        const EvolutionState q = gpu4.to_state();
+        bool pop_same = q.population.size() == r.population.size();
+        for (size_t i = 0; pop_same && i < r.population.size(); ++i)
+            pop_same = same_genome(q.population[i].genome, r.population[i].genome) &&
+                       q.population[i].fitness == r.population[i].fitness &&
+                       q.population[i].evaluated == r.population[i].evaluated;
+        report("ScriptedAdvisor in the loop: params history + GA stream identical",
+               ok && pop_same && fired >= 1 && worst <= 5e-2 && gpu4.rng_state() == r.rng.state(),
+               std::to_string(fired) + " of 10 generations with adjusted params, fitness before forcing rel " +
+                   std::to_string(worst));
     }
 
     // sharded GpuEvolution(cfg, rank, world, allreduce): two ranks in two
