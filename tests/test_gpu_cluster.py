@@ -131,6 +131,38 @@ def test_cluster_divergence_exit(vx, ctx, orc):
     assert out[1].diverged and not out[0].diverged
 
 
+@pytest.mark.parametrize("n,frac", [(7, 0.0), (7, 0.99), (8, 0.5), (10, 0.4), (10, 0.75), (10, 0.999)])
+def test_cluster_divergence_mid_run(vx, ctx, orc, n, frac):
+    """A mass leaves the +-1e6 box several steps into the run, in a chosen
+    CTA's range: the divergence word of that step reaches every CTA one phase
+    later (no cluster barrier per step), and every CTA stops with the state of
+    exactly that step, like step() (physics.hpp:260-263)."""
+    def mutate(pos, vel):
+        vel[int(frac * (len(vel) - 1)), 1] = 1.8e10  # ~1.8e5 m per step: out of the box at step ~5
+    out = _exit_case(vx, ctx, orc, n, mutate, 40)
+    assert out[1].diverged and 3 <= out[1].steps <= 8 and not out[0].diverged
+
+
+@pytest.mark.parametrize("n", [7, 8, 9, 10])
+def test_cluster_zero_length_every_size(vx, ctx, orc, n):
+    """Coincident masses in the first CTA's range: the zero-length verdict of
+    step 0 arrives one phase later and every CTA rolls its state back."""
+    def mutate(pos, vel):
+        pos[1] = pos[0]
+    out = _exit_case(vx, ctx, orc, n, mutate, 12)
+    assert out[1].diverged and out[1].spring_updates == 0 and out[1].steps == 1
+
+
+@pytest.mark.parametrize("steps", [1, 2, 3])
+def test_cluster_short_launches(vx, ctx, orc, steps):
+    """1-3 step launches: the last step's verdict and halo are drained after
+    the loop; a zero-length robot in the batch still rolls back."""
+    def mutate(pos, vel):
+        pos[-1] = pos[-2]
+    out = _exit_case(vx, ctx, orc, 10, mutate, steps)
+    assert out[1].diverged and out[1].spring_updates == 0 and not out[0].diverged
+
+
 def test_cluster_evaluate_fitness(vx, ctx, orc):
     """evaluate_fitness on 10^3 decodes runs the cluster kernel and agrees with
     the reference within the evaluate tolerance."""
