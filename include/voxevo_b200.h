@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define VX_ABI_VERSION 2
+#define VX_ABI_VERSION 3
 #define VX_MAX_HIDDEN 8
 #define VX_NMAT 5
 
@@ -384,7 +384,8 @@ vx_status vx_fp64_peak(vx_ctx* ctx, double* tflops);
 /* Self-check of the integrator's branch-free sqrt / reciprocal against the
  * IEEE sqrt(x) and 1.0/x over n pseudo-random inputs spanning the ranges the
  * integrator feeds them (plus powers of two and a few ulps around them);
- * mismatches[0] = sqrt, mismatches[1] = rcp. */
+ * mismatches[0] = sqrt, mismatches[1] = rcp, mismatches[2] = the fused
+ * sqrt + reciprocal (sqrt(s) and 1.0/sqrt(s) from one refined rsqrt). */
 vx_status vx_fastmath_check(vx_ctx* ctx, int64_t n, uint64_t seed, int64_t* mismatches);
 
 /* ------------------------------------------------------------- bench ---- */

@@ -198,7 +198,7 @@ def _lib():
                 "there is no CPU fallback")
         lib = C.CDLL(LIB_PATH)
         _declare(lib)
-        if lib.vx_abi_version() != 2:
+        if lib.vx_abi_version() != 3:
             raise DeviceUnavailable("libvoxevo_b200 ABI mismatch")
         _LIB = lib
     return _LIB
@@ -402,11 +402,11 @@ class Context:
         return float(t.value)
 
     def fastmath_check(self, n: int, seed: int = 1) -> tuple:
-        """Mismatches (sqrt, rcp) of the integrator's branch-free sqrt / reciprocal
-        vs IEEE sqrt and division over n samples."""
-        out = np.zeros(2, np.int64)
+        """Mismatches (sqrt, rcp, fused sqrt+rcp) of the integrator's branch-free
+        sqrt / reciprocal vs IEEE sqrt and division over n samples."""
+        out = np.zeros(3, np.int64)
         _check(_lib().vx_fastmath_check(self.h, n, seed, out.ctypes.data))
-        return int(out[0]), int(out[1])
+        return int(out[0]), int(out[1]), int(out[2])
 
     def info(self) -> dict:
         sm, clk = C.c_int32(), C.c_int32()

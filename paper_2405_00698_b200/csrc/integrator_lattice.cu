@@ -249,11 +249,11 @@ __global__ void __launch_bounds__(NMP, 1) lattice_kernel(LatArgs A) {
                 double dy = x1 - Xr[NMP + nb];
                 double dz = x2 - Xr[2 * NMP + nb];
                 const double len2 = dx * dx + dy * dy + dz * dz;
-                const double len = sqrt_rn_fast(len2);  // == sqrt(len2) on every used step (vx_internal.cuh)
+                double len, inv_len;  // RN(sqrt(len2)), RN(1 / len) (vx_internal.cuh)
+                    sqrt_rcp_rn_fast(len2, len, inv_len);
                 zero_len |= (valid && len2 < A.zero_len2) ? 1 : 0;  // <=> sqrt(len2) < kZeroLengthEps
                 const double r0 = PR[d * NMP + a];
                 const double rest = r0 + (SA[vox] * r0) * D[vox];
-                const double inv_len = rcp_rn_fast(len);
                 const double nx = dx * inv_len, ny = dy * inv_len, nz = dz * inv_len;
                 const double rel = (v0 - Xr[3 * NMP + nb]) * nx + (v1 - Xr[4 * NMP + nb]) * ny +
                                    (v2 - Xr[5 * NMP + nb]) * nz;
@@ -599,11 +599,11 @@ __global__ void __launch_bounds__(VertexGeom<N>::NT, 1) vertex_kernel(LatArgs A)
                 double dy = x1 - Xa[XS - off];
                 double dz = x2 - Xa[2 * XS - off];
                 const double len2 = dx * dx + dy * dy + dz * dz;
-                const double len = sqrt_rn_fast(len2);
+                double len, inv_len;  // RN(sqrt(len2)), RN(1 / len) (vx_internal.cuh)
+                    sqrt_rcp_rn_fast(len2, len, inv_len);
                 zero_len |= (valid && len2 < A.zero_len2) ? 1 : 0;
                 const double r0 = PR[d * NT + a];
                 const double rest = r0 + (SA[vox] * r0) * D[vox];
-                const double inv_len = rcp_rn_fast(len);
                 const double nx = dx * inv_len, ny = dy * inv_len, nz = dz * inv_len;
                 const double rel = (v0 - Xa[3 * XS - off]) * nx + (v1 - Xa[4 * XS - off]) * ny +
                                    (v2 - Xa[5 * XS - off]) * nz;

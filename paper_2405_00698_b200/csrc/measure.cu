@@ -44,7 +44,7 @@ __device__ double sample_range(uint64_t h, int emin, int emax) {
 }
 
 __global__ void fastmath_kernel(int64_t n, uint64_t seed, unsigned long long* bad) {
-    unsigned long long bs = 0, br = 0;
+    unsigned long long bs = 0, br = 0, bf = 0;
     for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         const uint64_t h = mix64(seed ^ static_cast<uint64_t>(i));
@@ -52,9 +52,16 @@ __global__ void fastmath_kernel(int64_t n, uint64_t seed, unsigned long long* ba
         const double x = sample_range(mix64(h), -31, 22);   // spring length: [1e-9, 4e6]
         if (__double_as_longlong(sqrt_rn_fast(s)) != __double_as_longlong(sqrt(s))) ++bs;
         if (__double_as_longlong(rcp_rn_fast(x)) != __double_as_longlong(1.0 / x)) ++br;
+        double len, inv;
+        sqrt_rcp_rn_fast(s, len, inv);
+        const double lref = sqrt(s);
+        if (__double_as_longlong(len) != __double_as_longlong(lref) ||
+            __double_as_longlong(inv) != __double_as_longlong(1.0 / lref))
+            ++bf;
     }
     if (bs) atomicAdd(bad, bs);
     if (br) atomicAdd(bad + 1, br);
+    if (bf) atomicAdd(bad + 2, bf);
 
 }
 
@@ -65,16 +72,17 @@ extern "C" {
 vx_status vx_fastmath_check(vx_ctx* ctx, int64_t n, uint64_t seed, int64_t* mismatches) {
     if (!ctx || !mismatches || n < 0) return VX_EINVAL;
     DevBuf<unsigned long long> bad;
-    VX_TRY(bad.alloc(2));
+    VX_TRY(bad.alloc(3));
     VX_TRY(bad.zero(ctx->stream));
     fastmath_kernel<<<ctx->sm_count * 8, 256, 0, ctx->stream>>>(n, seed, bad.p);
     ctx->launches++;
     VX_CUDA(cudaGetLastError());
-    unsigned long long h[2];
+    unsigned long long h[3];
     VX_CUDA(cudaMemcpyAsync(h, bad.p, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
     VX_CUDA(cudaStreamSynchronize(ctx->stream));
     mismatches[0] = static_cast<int64_t>(h[0]);
     mismatches[1] = static_cast<int64_t>(h[1]);
+    mismatches[2] = static_cast<int64_t>(h[2]);
 
     return VX_OK;
 }
