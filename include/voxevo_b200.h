@@ -139,6 +139,13 @@ void* vx_get_stream(vx_ctx* ctx);
 vx_status vx_synchronize(vx_ctx* ctx);
 /* Number of this library's kernel launches issued on ctx so far. */
 uint64_t vx_launch_count(vx_ctx* ctx);
+/* 10^3 cluster integrator: a persistent one-SM streaming filler on the SMs no
+ * 4-CTA cluster can be placed on (robots claimed from one shared counter).
+ * mode -1: from the VX_FILLER environment variable (default 1), 0 off,
+ * 1 on for batches large enough to keep the clusters busy, 2 on at any batch
+ * size (tests).  vx_last_filler_ctas: filler CTAs of the last launch. */
+vx_status vx_set_filler(vx_ctx* ctx, int32_t mode);
+int32_t vx_last_filler_ctas(vx_ctx* ctx);
 /* SM count / clock / name of the context device. */
 vx_status vx_device_info(vx_ctx* ctx, int32_t* sm_count, int32_t* clock_khz, char* name, int32_t name_cap);
 

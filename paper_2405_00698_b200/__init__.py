@@ -221,6 +221,8 @@ def _declare(lib):
         "vx_synchronize": (i32, [vp]),
         "vx_launch_count": (u64, [vp]),
         "vx_last_integrator": (i32, [vp]),
+        "vx_set_filler": (i32, [vp, i32]),
+        "vx_last_filler_ctas": (i32, [vp]),
         "vx_device_info": (i32, [vp, P(i32), P(i32), C.c_char_p, i32]),
         "vx_sample_genomes_dev": (i32, [vp, P(Arch), i32, vp, vp, vp]),
         "vx_decode_dev": (i32, [vp, P(Arch), i32, vp, vp, i32, i32, i32, vp, vp, vp]),
@@ -386,6 +388,16 @@ class Context:
         """Kernel of the last integrator launch: generic | lattice | cluster | stream."""
         k = int(_lib().vx_last_integrator(self.h))
         return {0: "generic", 1: "lattice", 2: "cluster", 3: "stream"}.get(k, "none")
+
+    def set_filler(self, mode: int):
+        """10^3 cluster integrator's one-SM filler on the SMs no 4-CTA cluster
+        can use: -1 from VX_FILLER (default on), 0 off, 1 on for large batches,
+        2 on at any batch size."""
+        _check(_lib().vx_set_filler(self.h, int(mode)), "vx_set_filler")
+
+    @property
+    def last_filler_ctas(self) -> int:
+        return int(_lib().vx_last_filler_ctas(self.h))
 
     def timing(self, on: bool = True):
         _check(_lib().vx_timing_enable(self.h, 1 if on else 0))

@@ -384,6 +384,12 @@ vx_status vx_synchronize(vx_ctx* ctx) {
 }
 uint64_t vx_launch_count(vx_ctx* ctx) { return ctx ? ctx->launches : 0; }
 int32_t vx_last_integrator(vx_ctx* ctx) { return ctx ? ctx->last_integrator : -1; }
+vx_status vx_set_filler(vx_ctx* ctx, int32_t mode) {
+    if (!ctx || mode < -1 || mode > 2) return VX_EINVAL;
+    ctx->filler_mode = mode;
+    return VX_OK;
+}
+int32_t vx_last_filler_ctas(vx_ctx* ctx) { return ctx ? ctx->filler_ctas : 0; }
 vx_status vx_device_info(vx_ctx* ctx, int32_t* sm_count, int32_t* clock_khz, char* name, int32_t name_cap) {
     if (!ctx) return VX_EINVAL;
     if (sm_count) *sm_count = ctx->sm_count;

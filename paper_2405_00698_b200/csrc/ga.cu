@@ -26,30 +26,43 @@ namespace {
 
 constexpr int kThreads = 256;
 
-__global__ void hist_kernel(int P, int cells, const uint8_t* __restrict__ mat, int64_t* __restrict__ hist,
-                            int accumulate) {
+// per-cell material counts over P grids: blocks tile (cell range x slice of
+// the population), one integer atomic per (cell, material) and block
+__global__ void hist_kernel(int P, int cells, const uint8_t* __restrict__ mat, int64_t* __restrict__ hist) {
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= cells) return;
-    int64_t n[VX_NMAT] = {0, 0, 0, 0, 0};
-    for (int a = 0; a < P; ++a) {
+    const int per = (P + gridDim.y - 1) / gridDim.y;
+    const int a0 = blockIdx.y * per, a1 = min(P, a0 + per);
+    if (a0 >= a1) return;
+    int n[VX_NMAT] = {0, 0, 0, 0, 0};
+    for (int a = a0; a < a1; ++a) {
         const int m = mat[static_cast<size_t>(a) * cells + c];
         if (m < VX_NMAT) n[m] += 1;
     }
-    for (int k = 0; k < VX_NMAT; ++k) hist[c * VX_NMAT + k] = (accumulate ? hist[c * VX_NMAT + k] : 0) + n[k];
+    for (int k = 0; k < VX_NMAT; ++k)
+        if (n[k])
+            atomicAdd(reinterpret_cast<unsigned long long*>(hist + c * VX_NMAT + k),
+                      static_cast<unsigned long long>(n[k]));
 }
 
 // counts over a list of individuals (this rank's share), as doubles for the
-// exchange-buffer all-reduce (exact: counts < 2^53)
+// exchange-buffer all-reduce: blocks tile (cell range x slice of the list),
+// each adds its slice's integer counts with one atomic per (cell, material)
+// (exact and order-free: counts < 2^53); `out` is zeroed first
 __global__ void hist_sel_kernel(int n, const int32_t* __restrict__ sel, int cells, const uint8_t* __restrict__ mat,
                                 double* __restrict__ out) {
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= cells) return;
-    int64_t cnt[VX_NMAT] = {0, 0, 0, 0, 0};
-    for (int q = 0; q < n; ++q) {
+    const int per = (n + gridDim.y - 1) / gridDim.y;
+    const int q0 = blockIdx.y * per, q1 = min(n, q0 + per);
+    if (q0 >= q1) return;
+    int cnt[VX_NMAT] = {0, 0, 0, 0, 0};
+    for (int q = q0; q < q1; ++q) {
         const int m = mat[static_cast<size_t>(sel[q]) * cells + c];
         if (m < VX_NMAT) cnt[m] += 1;
     }
-    for (int k = 0; k < VX_NMAT; ++k) out[c * VX_NMAT + k] = static_cast<double>(cnt[k]);
+    for (int k = 0; k < VX_NMAT; ++k)
+        if (cnt[k]) atomicAdd(out + c * VX_NMAT + k, static_cast<double>(cnt[k]));
 }
 
 __global__ void hist_from_doubles_kernel(int n, const double* __restrict__ in, int64_t* __restrict__ out) {
@@ -86,7 +99,12 @@ __global__ void diversity_kernel(int P, int cells, const int64_t* __restrict__ h
 
 vx_status histogram_dev(vx_ctx* ctx, int P, int cells, const uint8_t* d_mat, int64_t* d_hist, bool accumulate) {
     if (cells <= 0) return VX_OK;
-    hist_kernel<<<ceil_div(cells, kThreads), kThreads, 0, ctx->stream>>>(P, cells, d_mat, d_hist, accumulate ? 1 : 0);
+    if (!accumulate)
+        VX_CUDA(cudaMemsetAsync(d_hist, 0, static_cast<size_t>(cells) * VX_NMAT * sizeof(int64_t), ctx->stream));
+    if (P <= 0) return VX_OK;
+    const int bx = ceil_div(cells, kThreads);
+    const int by = std::max(1, std::min(ceil_div(P, 16), ceil_div(2 * ctx->sm_count * 8, bx)));
+    hist_kernel<<<dim3(bx, by), kThreads, 0, ctx->stream>>>(P, cells, d_mat, d_hist);
     ctx->launches++;
     VX_CUDA(cudaGetLastError());
     return VX_OK;
@@ -95,7 +113,12 @@ vx_status histogram_dev(vx_ctx* ctx, int P, int cells, const uint8_t* d_mat, int
 vx_status histogram_sel_dev(vx_ctx* ctx, int n_sel, const int32_t* d_sel, int cells, const uint8_t* d_mat,
                             double* d_out) {
     if (cells <= 0) return VX_OK;
-    hist_sel_kernel<<<ceil_div(cells, kThreads), kThreads, 0, ctx->stream>>>(n_sel, d_sel, cells, d_mat, d_out);
+    VX_CUDA(cudaMemsetAsync(d_out, 0, static_cast<size_t>(cells) * VX_NMAT * sizeof(double), ctx->stream));
+    if (n_sel <= 0) return VX_OK;
+    // ~2 waves of 256-thread blocks, >= 16 individuals per slice
+    const int bx = ceil_div(cells, kThreads);
+    const int by = std::max(1, std::min(ceil_div(n_sel, 16), ceil_div(2 * ctx->sm_count * 8, bx)));
+    hist_sel_kernel<<<dim3(bx, by), kThreads, 0, ctx->stream>>>(n_sel, d_sel, cells, d_mat, d_out);
     ctx->launches++;
     VX_CUDA(cudaGetLastError());
     return VX_OK;

@@ -29,10 +29,13 @@
 //    needed.
 // Compiled with --fmad=false; all sums in reference order.
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <string>
 #include <type_traits>
 
+#include "stream_sym.cuh"
 #include "vx_cluster.cuh"
 #include "vx_internal.cuh"
 
@@ -62,6 +65,14 @@ struct ClArgs {
     int halo;        // H: max backward mass-index offset of a lattice spring
     int vw, vh, ncell;
     double zero_len2;
+    // persistent 10^3 mode (claim non-null): robots are claimed from claim[0],
+    // shared with the one-SM filler the last cluster to start launches
+    int32_t* claim;  // [0] next robot [1] filler robots [2] clusters started, [4..] u64 timestamps
+    int n_robots;
+    int n_clusters;  // co-resident clusters of this launch
+    int n_fill;      // filler CTAs (0: none)
+    int fill_stop;   // the filler claims no robot once claim[0] reaches this
+    SymArgs fill;    // the filler's arguments (stream_sym.cuh)
 };
 
 __global__ void __launch_bounds__(kNmp, 1) cluster_kernel(ClArgs A) {
@@ -487,13 +498,13 @@ size_t cluster_vertex_smem() {
     return (6ull * G::XS + 65ull * kNmp + 2ull * (G::NCELL + 1)) * sizeof(double);
 }
 
+// one robot r on this cluster (every CTA of the cluster calls it with the same r)
 template <int N>
-__global__ void __launch_bounds__(kNmp, 1) cluster_vertex_kernel(ClArgs A) {
+__device__ __forceinline__ void cluster_vertex_robot(const ClArgs& A, const int r) {
     using G = ClusterGeom<N>;
     constexpr int CL = G::CL, Q = G::Q, PAD = G::PAD, XS = G::XS, VW = G::VW, NV = G::NV;
     constexpr int NTV = G::NCELL + 1;
     const uint32_t rank = cluster_rank();
-    const int r = blockIdx.x / CL;
     const BatchView& b = A.b;
     const int64_t mo = b.mass_off[r], so = b.spring_off[r];
     const int nm = b.nmass[r];
@@ -870,6 +881,50 @@ __global__ void __launch_bounds__(kNmp, 1) cluster_vertex_kernel(ClArgs A) {
     }
 }
 
+// Static: cluster blockIdx.x / CL integrates robot blockIdx.x / CL.
+// Persistent (A.claim set, grid = the co-resident cluster count, 10^3): every
+// cluster claims robots from the counter it shares with the one-SM filler
+// (stream_sym.cuh, stream_sym_filler); rank 0 draws and broadcasts through
+// DSMEM.  The last cluster to become resident launches the filler from the
+// device (dynamic parallelism, fire-and-forget), so its CTAs can only land on
+// the SMs no 4-CTA cluster was placed on; the cluster grid completes only
+// after its child grid.
+template <int N>
+__global__ void __launch_bounds__(kNmp, 1) cluster_vertex_kernel(ClArgs A) {
+    constexpr int CL = ClusterGeom<N>::CL;
+    if (!A.claim) {
+        cluster_vertex_robot<N>(A, static_cast<int>(blockIdx.x) / CL);
+        return;
+    }
+    __shared__ int s_robot;
+    const uint32_t rank = cluster_rank();
+    unsigned long long* tstat = reinterpret_cast<unsigned long long*>(A.claim + 4);  // [0] min start [1] max start [2] max end
+    if (rank == 0 && threadIdx.x == 0) {
+        const unsigned long long t = globaltimer_ns();
+        atomicMin(tstat, t);
+        atomicMax(tstat + 1, t);
+        if constexpr (N == 10) {
+            if (atomicAdd(A.claim + 2, 1) == A.n_clusters - 1 && A.n_fill > 0)
+                stream_sym_filler<10><<<A.n_fill, kStreamThreads, sym_filler_smem(), cudaStreamFireAndForget>>>(
+                    A.fill, A.claim, A.n_robots, A.fill_stop);
+        }
+    }
+    for (;;) {
+        cluster_barrier();  // every CTA done with the previous s_robot / robot
+        if (rank == 0 && threadIdx.x == 0) {
+            const int c = atomicAdd(A.claim, 1);
+            for (int q = 0; q < CL; ++q) st_remote_u32(map_rank(smem_addr(&s_robot), static_cast<uint32_t>(q)), c);
+        }
+        cluster_barrier();
+        const int r = s_robot;
+        if (r >= A.n_robots) {  // uniform over the cluster
+            if (rank == 0 && threadIdx.x == 0) atomicMax(tstat + 2, globaltimer_ns());
+            return;
+        }
+        cluster_vertex_robot<N>(A, r);
+    }
+}
+
 size_t cluster_smem(int ncell) { return (6ull * kXS + 65ull * kNmp + 2ull * (ncell + 1)) * sizeof(double); }
 
 int cluster_size_for(int nm_max) { return (nm_max + kNmp - 2) / (kNmp - 1); }
@@ -959,6 +1014,114 @@ vx_status integrate_cluster(vx_ctx* ctx, vx_batch* b, int64_t n_steps, bool writ
         ctx->launches++;
         return VX_OK;
     };
+    if (cluster_vertex_grid(b) == 10) {
+        ctx->filler_ctas = 0;
+        using G = ClusterGeom<10>;
+        const size_t smem = cluster_vertex_smem<10>();
+        int mode = ctx->filler_mode;
+        if (mode < 0) {
+            static const char* env = std::getenv("VX_FILLER");
+            mode = env ? std::atoi(env) : 1;
+        }
+        if (ctx->cluster_slots < 0) {  // co-resident 4-CTA clusters on this device
+            VX_CUDA(cudaFuncSetAttribute(cluster_vertex_kernel<10>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem)));
+            cudaLaunchConfig_t cfg{};
+            cfg.gridDim = dim3(G::CL);
+            cfg.blockDim = dim3(kNmp);
+            cfg.dynamicSmemBytes = smem;
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeClusterDimension;
+            attr[0].val.clusterDim.x = G::CL;
+            attr[0].val.clusterDim.y = 1;
+            attr[0].val.clusterDim.z = 1;
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+            int n = 0;
+            if (cudaOccupancyMaxActiveClusters(&n, cluster_vertex_kernel<10>, &cfg) != cudaSuccess) n = 0;
+            cudaGetLastError();
+            ctx->cluster_slots = n;
+        }
+        const int slots = ctx->cluster_slots;
+        const int idle = ctx->sm_count - slots * G::CL;
+        // a filler robot takes ~kFillerRatio cluster-robot times: the filler
+        // stops claiming while the clusters still have that much work left
+        static const char* ratio_env = std::getenv("VX_FILLER_RATIO");
+        const int ratio = ratio_env ? std::atoi(ratio_env) : 8;
+        const int64_t stop_at = static_cast<int64_t>(b->n) - static_cast<int64_t>(slots) * ratio;
+        const bool use = slots > 0 && idle > 0 &&
+                         ((mode == 1 && stop_at >= idle) || (mode == 2 && b->n > 0));
+        if (use) {
+            VX_TRY(ctx->claim.alloc(16));
+            VX_CUDA(cudaMemsetAsync(ctx->claim.p, 0, 16 * sizeof(int32_t), ctx->stream));
+            VX_CUDA(cudaMemsetAsync(ctx->claim.p + 4, 0xFF, sizeof(uint64_t), ctx->stream));   // min timestamps
+            VX_CUDA(cudaMemsetAsync(ctx->claim.p + 10, 0xFF, sizeof(uint64_t), ctx->stream));
+            static const char* ctas_env = std::getenv("VX_FILLER_CTAS");  // A/B: filler width (0: none)
+            int nfill = mode == 2 ? std::min(idle, std::max(1, b->n / 2)) : idle;
+            if (ctas_env) nfill = std::min(idle, std::max(0, std::atoi(ctas_env)));
+            const int stop = mode == 2 ? b->n : static_cast<int>(stop_at);
+            const int nclus = std::min(slots, b->n);
+            A.claim = ctx->claim.p;
+            A.n_robots = b->n;
+            A.n_clusters = nclus;
+            A.n_fill = nfill;
+            A.fill_stop = stop;
+            if (nfill > 0) {  // the filler's arguments and per-CTA scratch slots
+                SymArgs& F = A.fill;
+                F.b = A.b;
+                F.vkey = b->vkey.p;
+                F.act_vox = b->act_vox.p;
+                F.sign = b->sign.p;
+                F.amp = b->amp.p;
+                F.drive = ctx->drive.p;
+                F.sp = sp;
+                F.n_steps = n_steps;
+                F.write_back = write_back ? 1 : 0;
+                F.out = d_summaries;
+                F.zero_len2 = zero_len2;
+                F.zeta2 = b->uniform_zeta * 2.0;
+                F.mu = b->uniform_mass * b->uniform_mass / (b->uniform_mass + b->uniform_mass);
+                F.L = sym_layout<10>();
+                F.ntab_max = nullptr;
+                VX_TRY(ctx->filler_scratch.alloc(F.L.per_robot * static_cast<size_t>(nfill)));
+                F.scratch = ctx->filler_scratch.p;
+                VX_CUDA(cudaFuncSetAttribute(stream_sym_filler<10>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(sym_filler_smem())));
+            }
+            VX_CUDA(cudaFuncSetAttribute(cluster_vertex_kernel<10>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem)));
+            cudaLaunchConfig_t cfg{};
+            cfg.gridDim = dim3(static_cast<unsigned>(nclus * G::CL));
+            cfg.blockDim = dim3(kNmp);
+            cfg.dynamicSmemBytes = smem;
+            cfg.stream = ctx->stream;
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeClusterDimension;
+            attr[0].val.clusterDim.x = G::CL;
+            attr[0].val.clusterDim.y = 1;
+            attr[0].val.clusterDim.z = 1;
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+            VX_CUDA(cudaLaunchKernelEx(&cfg, cluster_vertex_kernel<10>, A));
+            ctx->launches += nfill > 0 ? 2 : 1;
+            static const char* stats_env = std::getenv("VX_FILLER_STATS");
+            if (stats_env && *stats_env == '1') {  // development aid: who did what, when
+                int32_t h[16];
+                VX_CUDA(cudaMemcpyAsync(h, ctx->claim.p, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+                VX_CUDA(cudaStreamSynchronize(ctx->stream));
+                uint64_t t[6];
+                std::memcpy(t, h + 4, sizeof(t));
+                const uint64_t t0 = t[0];
+                auto rel = [t0](uint64_t x) { return (x == ~0ull || x == 0) ? -1.0 : (static_cast<double>(x) - t0) * 1e-6; };
+                std::fprintf(stderr,
+                             "[filler] robots %d / %d, filler CTAs %d, stop_at %d | ms from first cluster start: "
+                             "last cluster start %.3f, first filler start %.3f, filler end %.3f, cluster end %.3f\n",
+                             h[1], b->n, nfill, stop, rel(t[1]), rel(t[3]), rel(t[4]), rel(t[2]));
+            }
+            ctx->filler_ctas = nfill;
+            return VX_OK;
+        }
+    }
     switch (cluster_vertex_grid(b)) {
         case 7: return launch(cluster_vertex_kernel<7>, ClusterGeom<7>::CL, cluster_vertex_smem<7>());
         case 8: return launch(cluster_vertex_kernel<8>, ClusterGeom<8>::CL, cluster_vertex_smem<8>());
