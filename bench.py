@@ -54,7 +54,8 @@ FLOPS_PER_UPDATE = 48  # 48 FP64 flop (+1 sqrt +1 div) per spr
 METRIC = "spring-mass updates/sec (1/2/4/8 B200) and generations/sec at fixed population"
 WORKLOADS = {
     "config3": dict(P=4096, grid=10, ref_P=64, cpu_sample=32,
-                    kernel="cluster_vertex_kernel<10> (4-CTA thread-block cluster per robot)",
+                    kernel="cluster_vertex_persistent<10> (33 persistent 4-CTA clusters, one robot at a time each) + its "
+                           "device-launched stream_sym_filler<10> on the 16 SMs no cluster can use",
                     traffic="cluster_traffic.json",
                     desc="config 3: population 4096 of 10x10x10 robots per GPU, successive generations of one run "
                          "(elite selection / crossover / mutation, 5000-step fitness)"),

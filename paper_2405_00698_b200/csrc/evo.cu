@@ -19,11 +19,14 @@
 // reference does.
 #include <algorithm>
 #include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <memory>
 #include <random>
 #include <sstream>
+#include <string>
 #include <thread>
 #include <vector>
 
@@ -95,6 +98,33 @@ void* pinned_alloc(size_t n) {
     return cudaMallocHost(&p, n) == cudaSuccess ? p : nullptr;
 }
 void pinned_free(void* p) { cudaFreeHost(p); }
+
+// a grow-only pinned host array (staging for async uploads)
+template <typename T>
+struct PinnedBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    PinnedBuf() = default;
+    PinnedBuf(const PinnedBuf&) = delete;
+    PinnedBuf& operator=(const PinnedBuf&) = delete;
+    ~PinnedBuf() {
+        if (p) cudaFreeHost(p);
+    }
+    vx_status alloc(size_t count) {
+        if (count <= n) return VX_OK;
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        n = 0;
+        const size_t want = count + count / 4;  // headroom: cudaFreeHost on a regrow can wait for the device
+        const cudaError_t err = cudaMallocHost(reinterpret_cast<void**>(&p), want * sizeof(T));
+        if (err != cudaSuccess) {
+            p = nullptr;
+            return cuda_status(err, "cudaMallocHost");
+        }
+        n = want;
+        return VX_OK;
+    }
+};
 }  // namespace
 
 struct vx_evo {
@@ -122,7 +152,15 @@ struct vx_evo {
     std::vector<ChildPlan> h_plan;
     std::vector<uint32_t> h_masks;
     MutStore h_mut{pinned_alloc, pinned_free};
-    cudaEvent_t mut_uploaded = nullptr;  // the previous plan's async upload has read h_mut
+    // the plan thread uploads its own result on up_stream as soon as the
+    // scan is done (overlapping the GPU evaluate); finish() only makes the
+    // breeding wait for `mut_uploaded` on the device
+    cudaStream_t up_stream = nullptr;
+    cudaEvent_t mut_uploaded = nullptr;  // the plan's async upload has read h_mut / the pinned staging
+    PinnedBuf<ChildPlan> hp_plan;        // pinned staging of h_plan / h_masks for that upload
+    PinnedBuf<uint32_t> hp_masks;
+    vx_status plan_upload_status = VX_OK;
+    std::string plan_upload_error;
     int64_t mask_words = 0;
     int plan_elite = 0;
     std::thread plan_thread;
@@ -142,6 +180,7 @@ struct vx_evo {
     std::vector<int32_t> todo;
     int rank = 0, world = 1;
     std::chrono::steady_clock::time_point t0;
+    std::chrono::steady_clock::time_point t_plan_done;  // the plan thread's end (VX_EVO_TRACE)
     vx_materials table{};
     double* ext_xbuf = nullptr;  // caller-owned exchange buffer (NCCL all-reduce operand)
     double* xb() { return ext_xbuf ? ext_xbuf : xbuf.p; }
@@ -154,7 +193,9 @@ struct vx_evo {
 
     ~vx_evo() {
         if (plan_thread.joinable()) plan_thread.join();
+        if (up_stream) cudaStreamSynchronize(up_stream);
         if (mut_uploaded) cudaEventDestroy(mut_uploaded);
+        if (up_stream) cudaStreamDestroy(up_stream);
     }
 };
 
@@ -163,6 +204,43 @@ namespace {
 // exchange buffer: [fitness P | spring updates P | material histogram cells x NMAT]
 size_t xbuf_doubles(const vx_evo* e) {
     return 2 * static_cast<size_t>(e->P) + static_cast<size_t>(e->cells) * VX_NMAT;
+}
+
+// The plan's device copy, issued by the plan thread on up_stream: rows and
+// masks through pinned staging, mutation entries straight from MutStore's
+// pinned slabs (one copy per run of chunks in one slab); mut_uploaded marks
+// the end.  The device buffers only grow, and nothing reads them until the
+// breeding of this generation (after the previous one's final sync).
+vx_status upload_plan(vx_evo* e) {
+    cudaStream_t s = e->up_stream;
+    const int n_child = e->P - e->plan_elite;
+    // grow with 25% headroom: a regrow's cudaFree would wait for the running
+    // integrator, and the hit count varies a little from generation to generation
+    auto grow = [](auto& buf, size_t need) { return need <= buf.n ? VX_OK : buf.alloc(need + need / 4); };
+    VX_TRY(grow(e->d_plan, static_cast<size_t>(std::max(1, n_child))));
+    VX_TRY(grow(e->d_masks, std::max<size_t>(1, e->h_masks.size())));
+    VX_TRY(grow(e->d_mut, std::max<size_t>(1, e->h_mut.size())));
+    if (n_child > 0) {
+        VX_TRY(e->hp_plan.alloc(static_cast<size_t>(n_child)));
+        std::memcpy(e->hp_plan.p, e->h_plan.data(), n_child * sizeof(ChildPlan));
+        VX_CUDA(cudaMemcpyAsync(e->d_plan.p, e->hp_plan.p, n_child * sizeof(ChildPlan), cudaMemcpyHostToDevice, s));
+    }
+    if (!e->h_masks.empty()) {
+        VX_TRY(e->hp_masks.alloc(e->h_masks.size()));
+        std::memcpy(e->hp_masks.p, e->h_masks.data(), e->h_masks.size() * sizeof(uint32_t));
+        VX_CUDA(cudaMemcpyAsync(e->d_masks.p, e->hp_masks.p, e->h_masks.size() * sizeof(uint32_t),
+                                cudaMemcpyHostToDevice, s));
+    }
+    for (size_t j = 0, nch = e->h_mut.chunks(); j < nch;) {
+        size_t k = j + 1;
+        while (k < nch && e->h_mut.continues(k)) ++k;
+        const size_t count = (k - 1 - j) * MutStore::kChunk + e->h_mut.chunk_size(k - 1);
+        VX_CUDA(cudaMemcpyAsync(e->d_mut.p + j * MutStore::kChunk, e->h_mut.chunk(j), count * sizeof(MutEntry),
+                                cudaMemcpyHostToDevice, s));
+        j = k;
+    }
+    VX_CUDA(cudaEventRecord(e->mut_uploaded, s));
+    return VX_OK;
 }
 
 // Breeding loop (evolution.hpp:267-289) in rank space: consumes the GA
@@ -176,7 +254,10 @@ void parse_plan(vx_evo* e) {
         plan_scan(e->rng, a, e->h_plan, e->h_masks, e->h_mut);
     } catch (const std::bad_alloc&) {
         e->plan_failed = true;
+        return;
     }
+    e->plan_upload_status = upload_plan(e);
+    if (e->plan_upload_status != VX_OK) e->plan_upload_error = vx_last_error();
 }
 
 vx_status validate_cfg(const vx_evo_config* c) {
@@ -225,8 +306,9 @@ vx_status alloc_evo(vx_evo* e) {
 }
 
 void start_plan(vx_evo* e) {
-    // the previous generation's upload reads h_mut asynchronously
+    // the previous plan's upload reads h_mut and the staging asynchronously
     if (e->mut_uploaded) cudaEventSynchronize(e->mut_uploaded);
+    e->plan_upload_status = VX_OK;
     e->plan_running = true;
     e->plan_failed = false;
     const int device = e->ctx->device;
@@ -235,6 +317,7 @@ void start_plan(vx_evo* e) {
         // not in a fresh one on device 0 (a new host thread starts there)
         cudaSetDevice(device);
         parse_plan(e);
+        e->t_plan_done = std::chrono::steady_clock::now();
     });
 }
 
@@ -272,6 +355,8 @@ vx_status vx_evo_create(vx_ctx* ctx, const vx_evo_config* cfg, vx_evo** out) {
     e->np = param_count(&cfg->arch);
     e->nb = 3LL * cfg->arch.m;
     VX_TRY(alloc_evo(e.get()));
+    VX_CUDA(cudaStreamCreateWithFlags(&e->up_stream, cudaStreamNonBlocking));
+    VX_CUDA(cudaEventCreateWithFlags(&e->mut_uploaded, cudaEventDisableTiming));
     // init_evolution (evolution.hpp:197-211): per-genome seeds from the master
     // stream, genomes sampled on device (K14)
     e->rng.seed(cfg->seed);
@@ -440,6 +525,7 @@ vx_status vx_evo_finish(vx_evo* e, vx_report* rep) {
     if (!e->begun) return (set_error("vx_evo_finish without vx_evo_begin"), VX_ESTATE);
     vx_ctx* ctx = e->ctx;
     const int c = e->cur, nx = 1 - c, P = e->P;
+    const auto t_fin0 = std::chrono::steady_clock::now();
     VX_TRY(merge_dev(ctx, static_cast<int>(e->todo.size()), e->d_todo.p, e->xb(), e->fit[c].p, e->ev[c].p));
     VX_TRY(sort_stats_dev(ctx, P, e->fit[c].p, e->perm.p, e->sorted.p, e->iota.p, e->keys_tmp.p, e->stats.p));
     VX_TRY(hist_from_doubles_dev(ctx, e->cells, e->xb() + 2 * P, e->hist.p));  // summed over ranks
@@ -476,29 +562,26 @@ vx_status vx_evo_finish(vx_evo* e, vx_report* rep) {
     for (int32_t a : e->todo) total += static_cast<uint64_t>(upd[a]);
     r.spring_updates = total;
     // breed (evolution.hpp:267-289)
+    static const bool trace = [] {
+        const char* v = std::getenv("VX_EVO_TRACE");  // development aid: where finish() waits
+        return v && *v == '1';
+    }();
+    const auto t_join0 = std::chrono::steady_clock::now();
     join_plan(e);
+    const auto t_join1 = std::chrono::steady_clock::now();
     if (e->plan_failed) return (set_error("breeding plan: host allocation failed"), VX_EOOM);
-    const int n_elite = e->plan_elite;
-    const int n_child = P - n_elite;
-    VX_TRY(e->d_plan.alloc(std::max(1, n_child)));
-    VX_TRY(e->d_masks.alloc(std::max<size_t>(1, e->h_masks.size())));
-    VX_TRY(e->d_mut.alloc(std::max<size_t>(1, e->h_mut.size())));
-    if (n_child > 0)
-        VX_CUDA(cudaMemcpyAsync(e->d_plan.p, e->h_plan.data(), n_child * sizeof(ChildPlan), cudaMemcpyHostToDevice,
-                                ctx->stream));
-    if (!e->h_masks.empty())
-        VX_CUDA(cudaMemcpyAsync(e->d_masks.p, e->h_masks.data(), e->h_masks.size() * sizeof(uint32_t),
-                                cudaMemcpyHostToDevice, ctx->stream));
-    for (size_t j = 0, nch = e->h_mut.chunks(); j < nch;) {  // pinned chunks: true async copies, one per run
-        size_t k = j + 1;                                      // of chunks in one pinned slab
-        while (k < nch && e->h_mut.continues(k)) ++k;
-        const size_t count = (k - 1 - j) * MutStore::kChunk + e->h_mut.chunk_size(k - 1);
-        VX_CUDA(cudaMemcpyAsync(e->d_mut.p + j * MutStore::kChunk, e->h_mut.chunk(j), count * sizeof(MutEntry),
-                                cudaMemcpyHostToDevice, ctx->stream));
-        j = k;
+    if (e->plan_upload_status != VX_OK) {
+        set_error(e->plan_upload_error.c_str());
+        return e->plan_upload_status;
     }
-    if (!e->mut_uploaded) VX_CUDA(cudaEventCreateWithFlags(&e->mut_uploaded, cudaEventDisableTiming));
-    VX_CUDA(cudaEventRecord(e->mut_uploaded, ctx->stream));
+    const int n_elite = e->plan_elite;
+    // the plan thread's upload (up_stream) before the breeding reads it
+    VX_CUDA(cudaStreamWaitEvent(ctx->stream, e->mut_uploaded, 0));
+    std::chrono::steady_clock::time_point t_up = t_join1, t_br = t_join1;
+    if (trace) {  // attribute the wait: uploads drained
+        VX_CUDA(cudaStreamSynchronize(ctx->stream));
+        t_up = std::chrono::steady_clock::now();
+    }
     BreedArgs A{};
     A.n_elite = n_elite;
     A.np = e->np;
@@ -521,6 +604,10 @@ vx_status vx_evo_finish(vx_evo* e, vx_report* rep) {
     A.dst_grid = e->grid[nx].p;
     A.dst_gridw = e->gw[nx].p;
     VX_TRY(breed_dev(ctx, A, P, e->d_mut.p, static_cast<int64_t>(e->h_mut.size())));
+    if (trace) {
+        VX_CUDA(cudaStreamSynchronize(ctx->stream));
+        t_br = std::chrono::steady_clock::now();
+    }
     // host mirrors: elites are evaluated and keep their grids (and owners);
     // children are fresh
     std::vector<int32_t> elite_src(static_cast<size_t>(n_elite));
@@ -539,6 +626,14 @@ vx_status vx_evo_finish(vx_evo* e, vx_report* rep) {
     ++e->generation;
     e->begun = false;
     VX_CUDA(cudaStreamSynchronize(ctx->stream));  // host plan buffers are reused next generation
+    if (trace) {
+        const auto t_end = std::chrono::steady_clock::now();
+        auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+        std::fprintf(stderr, "[evo] gen %lld: plan ready %.3f ms after begin, finish: stats %.3f ms, plan wait %.3f ms, "
+                             "upload %.3f ms, breed %.3f ms, host tail %.3f ms, mutations %zu\n",
+                     static_cast<long long>(e->generation - 1), ms(e->t0, e->t_plan_done), ms(t_fin0, t_join0),
+                     ms(t_join0, t_join1), ms(t_join1, t_up), ms(t_up, t_br), ms(t_br, t_end), e->h_mut.size());
+    }
     r.wall_time = std::chrono::duration<double>(std::chrono::steady_clock::now() - e->t0).count();
     if (rep) *rep = r;
     return VX_OK;

@@ -891,11 +891,12 @@ __device__ __forceinline__ void cluster_vertex_robot(const ClArgs& A, const int 
 // after its child grid.
 template <int N>
 __global__ void __launch_bounds__(kNmp, 1) cluster_vertex_kernel(ClArgs A) {
+    cluster_vertex_robot<N>(A, static_cast<int>(blockIdx.x) / ClusterGeom<N>::CL);
+}
+
+template <int N>
+__global__ void __launch_bounds__(kNmp, 1) cluster_vertex_persistent(ClArgs A) {
     constexpr int CL = ClusterGeom<N>::CL;
-    if (!A.claim) {
-        cluster_vertex_robot<N>(A, static_cast<int>(blockIdx.x) / CL);
-        return;
-    }
     __shared__ int s_robot;
     const uint32_t rank = cluster_rank();
     unsigned long long* tstat = reinterpret_cast<unsigned long long*>(A.claim + 4);  // [0] min start [1] max start [2] max end
@@ -1024,7 +1025,7 @@ vx_status integrate_cluster(vx_ctx* ctx, vx_batch* b, int64_t n_steps, bool writ
             mode = env ? std::atoi(env) : 1;
         }
         if (ctx->cluster_slots < 0) {  // co-resident 4-CTA clusters on this device
-            VX_CUDA(cudaFuncSetAttribute(cluster_vertex_kernel<10>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            VX_CUDA(cudaFuncSetAttribute(cluster_vertex_persistent<10>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem)));
             cudaLaunchConfig_t cfg{};
             cfg.gridDim = dim3(G::CL);
@@ -1038,7 +1039,7 @@ vx_status integrate_cluster(vx_ctx* ctx, vx_batch* b, int64_t n_steps, bool writ
             cfg.attrs = attr;
             cfg.numAttrs = 1;
             int n = 0;
-            if (cudaOccupancyMaxActiveClusters(&n, cluster_vertex_kernel<10>, &cfg) != cudaSuccess) n = 0;
+            if (cudaOccupancyMaxActiveClusters(&n, cluster_vertex_persistent<10>, &cfg) != cudaSuccess) n = 0;
             cudaGetLastError();
             ctx->cluster_slots = n;
         }
@@ -1088,7 +1089,7 @@ vx_status integrate_cluster(vx_ctx* ctx, vx_batch* b, int64_t n_steps, bool writ
                 VX_CUDA(cudaFuncSetAttribute(stream_sym_filler<10>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              static_cast<int>(sym_filler_smem())));
             }
-            VX_CUDA(cudaFuncSetAttribute(cluster_vertex_kernel<10>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            VX_CUDA(cudaFuncSetAttribute(cluster_vertex_persistent<10>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem)));
             cudaLaunchConfig_t cfg{};
             cfg.gridDim = dim3(static_cast<unsigned>(nclus * G::CL));
@@ -1102,7 +1103,7 @@ vx_status integrate_cluster(vx_ctx* ctx, vx_batch* b, int64_t n_steps, bool writ
             attr[0].val.clusterDim.z = 1;
             cfg.attrs = attr;
             cfg.numAttrs = 1;
-            VX_CUDA(cudaLaunchKernelEx(&cfg, cluster_vertex_kernel<10>, A));
+            VX_CUDA(cudaLaunchKernelEx(&cfg, cluster_vertex_persistent<10>, A));
             ctx->launches += nfill > 0 ? 2 : 1;
             static const char* stats_env = std::getenv("VX_FILLER_STATS");
             if (stats_env && *stats_env == '1') {  // development aid: who did what, when

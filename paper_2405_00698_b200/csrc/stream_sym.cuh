@@ -46,6 +46,8 @@ struct SymGeom {
     static constexpr int PAD = VW * VW + VW + 1;
     static constexpr int PC = NVP + PAD;              // parameter columns (forward reads reach key + PAD)
     static constexpr int XS = PAD + NVP + PAD;        // state row stride: far entries on both sides
+    // shared-memory state (the filler): rows cover the keys of warps that hold a vertex
+    static constexpr int XSS = PAD + (NV + 31) / 32 * 32 + PAD;
     static constexpr int NCELL = N * N * N;
 };
 
@@ -240,11 +242,13 @@ __global__ void __launch_bounds__(1024) stream_sym_prep_kernel(SymArgs A) {
 #endif
 constexpr int kSymDBuf = VX_SYM_DBUF ? 2 : 1;
 
-// one robot's n_steps from its prepared scratch
-template <int N>
+// one robot's n_steps from its prepared scratch; kSmemX: the double-buffered
+// state lives in shared memory (rows of XSS) instead of the HBM scratch
+template <int N, bool kSmemX = false>
 __device__ void sym_robot(const SymArgs& A, int r, unsigned char* base) {
     using G = SymGeom<N>;
-    constexpr int PCOL = G::PC, NVP = G::NVP, XS = G::XS, PAD = G::PAD, VW = G::VW, T = G::T, MPT = G::MPT;
+    constexpr int PCOL = G::PC, NVP = G::NVP, XS = kSmemX ? G::XSS : G::XS, PAD = G::PAD, VW = G::VW, T = G::T,
+                  MPT = G::MPT;
     constexpr int NV = G::NV;
     const BatchView& b = A.b;
     constexpr SymLayout L = sym_layout<N>();
@@ -260,12 +264,22 @@ __device__ void sym_robot(const SymArgs& A, int r, unsigned char* base) {
     const double* SPH = at<double>(base, L.sph);
     double* Xc = at<double>(base, L.x0);
     double* Xn = at<double>(base, L.x1);
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    if constexpr (kSmemX) {  // both buffers from the prepared (far-initialised) HBM state
+        double* S = reinterpret_cast<double*>(smem_raw);
+        for (int q = t; q < 6 * XS; q += T) {
+            const int c = q / XS, k = q - c * XS;
+            S[q] = S[6 * XS + q] = Xc[c * G::XS + k];
+        }
+        Xc = S;
+        Xn = S + 6 * XS;
+        __syncthreads();
+    }
     const int64_t mo = b.mass_off[r];
     const int nm = b.nmass[r];
     vx_summary* out = A.out ? A.out + r : nullptr;
 
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    double* D = reinterpret_cast<double*>(smem_raw);  // [kSymDBuf][NT] drive per actuator row
+    double* D = reinterpret_cast<double*>(smem_raw) + (kSmemX ? 12 * XS : 0);  // [kSymDBuf][NT] drive per actuator row
     double* SA = D + kSymDBuf * NT;                    // [NT]
     __shared__ double s_maxsq[32];
 
@@ -510,8 +524,14 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_sym_kernel(SymArgs A
 
 // dynamic shared memory of the filler: single- or double-buffered drive table
 // plus the amplitude table, sized for any actuator count
+// plus (VX_FILLER_SMEMX, default on) the double-buffered state
+#ifndef VX_FILLER_SMEMX
+#define VX_FILLER_SMEMX 1
+#endif
+constexpr bool kFillerSmemX = VX_FILLER_SMEMX != 0;
 __host__ __device__ constexpr size_t sym_filler_smem() {
-    return (kSymDBuf + 1ull) * (SymGeom<10>::NCELL + 1) * sizeof(double);
+    return ((kFillerSmemX ? 12ull * SymGeom<10>::XSS : 0ull) + (kSymDBuf + 1ull) * (SymGeom<10>::NCELL + 1)) *
+           sizeof(double);
 }
 
 // Persistent filler: robots claimed one at a time from the counter the
@@ -540,7 +560,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_sym_filler(SymArgs A
         if (threadIdx.x == 0) atomicAdd(claim + 1, 1);
         sym_prep_robot<N>(A, r, base);
         __syncthreads();
-        sym_robot<N>(A, r, base);
+        sym_robot<N, kFillerSmemX>(A, r, base);
         __syncthreads();
     }
     if (threadIdx.x == 0) atomicMax(tstat + 4, globaltimer_ns());

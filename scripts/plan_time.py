@@ -3,7 +3,7 @@ sys.path.insert(0, os.environ.get("GRAFT_REPO_ROOT", "/root/repo"))
 import torch
 import paper_2405_00698_b200 as vx
 ctx = vx.Context(0)
-for world in (1, 2, 4, 8):
+for world in [int(w) for w in os.environ.get("WORLDS", "1,2,4,8").split(",")]:
     P = 256 * world
     cfg = vx.EvolutionConfig(population=P, grid=(6, 6, 6), seed=42, sim=vx.SimConfig(duration=5000 * 1e-5))
     st = vx.init_evolution(cfg, ctx)
