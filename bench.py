@@ -398,6 +398,16 @@ def main():
                     "peak_source": peak_src,
                     "algorithmic": f"{ab} B per spring update (SURVEY.md §8(d)) x {upd_per_launch:.4g} updates per "
                                    "launch"}
+        mb = meta.get("dram_bytes_per_update")  # measured (ncu dram__bytes) per update, same kernel
+        if mb and int_n and roofline["traffic"] is None:
+            roofline["traffic"] = mb * upd_per_launch  # the capture's bytes/update x this launch's updates
+        if mb and int_n:
+            ach_m = mb * upd_per_launch / (avg_int_ms * 1e-3) / 1e9
+            roofline.update({"achieved_measured_dram": ach_m, "frac_measured_dram": ach_m / peak_gbs,
+                             "dram_bytes_per_update_ncu": mb,
+                             "fp64_pipe_busy_ncu": meta.get("fp64_pipe_pct"),
+                             "note": "the kernel evaluates every spring from both endpoints (no force slots): "
+                                     "FP64-issue and L2-latency bound, see DESIGN.md §3 (streaming integrator)"})
     else:
         achieved = FLOPS_PER_UPDATE * upd_per_launch / (avg_int_ms * 1e-3) / 1e12 if int_n else None
         peak = ctx.fp64_peak_tflops()
