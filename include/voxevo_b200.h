@@ -171,12 +171,20 @@ vx_status vx_forward(vx_ctx* ctx, const vx_arch* a, int32_t P, const double* par
                      int32_t n_points, const double* points, double* probs, double* weight);
 /* decode for P genomes (morphology.hpp:141-157 over forward, genome.hpp:187-211):
  * materials (u8, argmax strict-> ties low) and clamped weights per cell,
- * cells in x-fastest order.  d_guard (optional, 1 u32) counts voxels whose top-2
- * softmax gap is < 1e-12 (argmax could differ from glibc's). */
+ * cells in x-fastest order.  The MLP layers run on the FP64 tensor pipe (DMMA);
+ * a genome with any voxel whose top-2 probability gap is < 1e-8 (relative) is
+ * re-decoded in the reference's sequential order, so materials equal the exact
+ * path's (VX_DECODE=exact in the environment forces the exact path).  d_guard
+ * (optional, 1 u32) counts voxels whose top-2 softmax gap is < 1e-12 (argmax
+ * could differ from glibc's). */
 vx_status vx_decode_dev(vx_ctx* ctx, const vx_arch* a, int32_t P, const double* d_params, const double* d_bmat,
                         int32_t w, int32_t h, int32_t d, uint8_t* d_mat, double* d_weight, uint32_t* d_guard);
 vx_status vx_decode(vx_ctx* ctx, const vx_arch* a, int32_t P, const double* params, const double* bmat, int32_t w,
                     int32_t h, int32_t d, uint8_t* mat, double* weight);
+/* How many genomes of the context's LAST decode launch were re-decoded on the
+ * exact path (-1: that decode ran on the exact path only).  Synchronises the
+ * context stream. */
+vx_status vx_decode_refined(vx_ctx* ctx, int64_t* n_refined);
 /* largest_component for P grids (morphology.hpp:162-208) */
 vx_status vx_largest_component_dev(vx_ctx* ctx, int32_t P, int32_t w, int32_t h, int32_t d, const uint8_t* d_in,
                                    uint8_t* d_out);

@@ -227,6 +227,7 @@ def _declare(lib):
         "vx_sample_genomes_dev": (i32, [vp, P(Arch), i32, vp, vp, vp]),
         "vx_decode_dev": (i32, [vp, P(Arch), i32, vp, vp, i32, i32, i32, vp, vp, vp]),
         "vx_decode": (i32, [vp, P(Arch), i32, vp, vp, i32, i32, i32, vp, vp]),
+        "vx_decode_refined": (i32, [vp, P(C.c_int64)]),
         "vx_largest_component_dev": (i32, [vp, i32, i32, i32, i32, vp, vp]),
         "vx_largest_component": (i32, [vp, i32, i32, i32, i32, vp, vp]),
         "vx_batch_build_dev": (i32, [vp, i32, i32, i32, i32, vp, vp, P(MaterialTable), P(GroundPlane), P(vp)]),
@@ -450,6 +451,16 @@ def decode(genomes_params: np.ndarray, genomes_bmat: np.ndarray, arch: Arch, w: 
     wt = np.zeros((P, cells))
     _check(_lib().vx_decode(ctx.h, C.byref(arch), P, _ptr(params), _ptr(bmat), w, h, d, _ptr(mat), _ptr(wt)), "decode")
     return mat, wt
+
+
+def decode_refined(ctx: Optional[Context] = None) -> int:
+    """Genomes of the context's last decode that the tensor-pipe path handed to
+    the exact sequential path (a top-2 gap < 1e-8); -1 if that decode ran on
+    the exact path only (VX_DECODE=exact, forward(), or weights too large)."""
+    ctx = ctx or default_context()
+    n = C.c_int64(0)
+    _check(_lib().vx_decode_refined(ctx.h, C.byref(n)), "decode_refined")
+    return int(n.value)
 
 
 def gaussian_encode(v, bmat: np.ndarray, m: int) -> np.ndarray:

@@ -92,6 +92,20 @@ vx_status vx_decode(vx_ctx* ctx, const vx_arch* a, int32_t P, const double* para
     return VX_OK;
 }
 
+vx_status vx_decode_refined(vx_ctx* ctx, int64_t* n_refined) {
+    if (!ctx || !n_refined) return VX_EINVAL;
+    *n_refined = -1;
+    if (ctx->decode_fix_n < 0) return VX_OK;
+    std::vector<uint8_t> f(static_cast<size_t>(ctx->decode_fix_n));
+    if (!f.empty())
+        VX_CUDA(cudaMemcpyAsync(f.data(), ctx->decode_fix.p, f.size(), cudaMemcpyDeviceToHost, ctx->stream));
+    VX_CUDA(cudaStreamSynchronize(ctx->stream));
+    int64_t n = 0;
+    for (uint8_t v : f) n += v != 0;
+    *n_refined = n;
+    return VX_OK;
+}
+
 vx_status vx_largest_component_dev(vx_ctx* ctx, int32_t P, int32_t w, int32_t h, int32_t d, const uint8_t* d_in,
                                    uint8_t* d_out) {
     if (!ctx || P < 0 || w < 1 || h < 1 || d < 1) return VX_EINVAL;

@@ -15,14 +15,16 @@
 //    lowest material), stable sigmoid + both clamps, and a guard counter for
 //    voxels whose top-2 probability gap is < 1e-12 (where device vs glibc
 //    transcendentals could flip the argmax — never observed).
-// FP64 is the reference's precision; tcgen05 has no f64 kind and B200 runs
-// DMMA at the FP64 vector rate, so the CUDA-core form with exact ordering is
-// used (decode is < 1% of a generation).
+// This exact-order kernel serves forward() point queries, VX_DECODE=exact, the
+// fix-up of near-tie genomes and architectures too large for the tensor path;
+// decode() runs decode_mma_kernel (below: the MLP layers on DMMA) first.
 //
 // K14 replaces sample_genome (genome.hpp:146-166): one warp per genome runs
 // its own mt19937_64 (warp-parallel twist, smem state), W entries are exact
 // uniform draws; B uses device log/cos (ulp-level vs glibc).
 #include <cmath>
+#include <cstdlib>
+#include <cstring>
 
 #include "vx_internal.cuh"
 
@@ -67,6 +69,8 @@ struct DecodeArgs {
     const double* points;
     double* probs;
     int n_points;
+    // fix-up launch after decode_mma_kernel: only CTAs whose flag is set run
+    const uint8_t* fix_only;
 };
 
 __device__ __forceinline__ double stable_sigmoid(double z) {
@@ -83,6 +87,7 @@ __device__ __forceinline__ double stable_sigmoid(double z) {
 }
 
 __global__ void __launch_bounds__(kThreads) decode_kernel(DecodeArgs A) {
+    if (A.fix_only && !A.fix_only[blockIdx.x]) return;
     const int g = A.select ? A.select[blockIdx.x] : static_cast<int>(blockIdx.x);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -198,6 +203,192 @@ __global__ void __launch_bounds__(kThreads) decode_kernel(DecodeArgs A) {
             }
         }
         __syncthreads();
+    }
+}
+
+// ------------------------------------------------- K2 on the FP64 tensor pipe
+// decode_mma_kernel: the same decode with every affine layer (genome.hpp:118-126)
+// as a [voxels x in] x [in x out] product on DMMA (mma.sync m8n8k4 .f64 —
+// tcgen05 has no f64 kind, so this is sm_100a's FP64 tensor path).
+//  * weights are re-laid into shared memory in FRAGMENT order (layer, n-tile,
+//    k-step, lane), zero-padded to 8-column / 4-deep tiles, so every B load is
+//    one conflict-free 256 B wavefront pair; biases seed the accumulators;
+//  * activations stay [feature][voxel] with a 36-double row stride (32 voxels
+//    + 4): A loads and C stores hit every bank pair exactly twice;
+//  * padded output columns come out exactly 0 (zero weights, zero bias,
+//    tanh(0) = 0), which is the next layer's zero K padding.
+// DMMA accumulates in a different order than the reference's sequential
+// acc += w*x, so logits differ by ulps.  Materials are made bit-identical to
+// the exact kernel BY CONSTRUCTION: a voxel whose top-2 probability gap is
+// below kFixGap (orders of magnitude above any DMMA-vs-sequential logit
+// difference) flags its genome, and decode_kernel re-decodes flagged genomes
+// with the exact sequential order (a fix-up launch whose unflagged CTAs exit).
+constexpr int kMmaMT = 4;                    // m-tiles of 8 voxels per tile
+constexpr int kMmaTile = kMmaMT * 8;         // 32 voxels per tile
+constexpr int kXS = kMmaTile + 4;            // activation row stride (doubles)
+constexpr double kFixGap = 1e-8;             // relative top-2 gap that forces the exact path
+
+struct MmaLayout {  // shared-memory offsets (doubles), host-computed
+    int nl;                                  // nh hidden layers + 1 head
+    int in[VX_MAX_HIDDEN + 1], out[VX_MAX_HIDDEN + 1];
+    int64_t src_w[VX_MAX_HIDDEN + 1], src_b[VX_MAX_HIDDEN + 1];  // offsets into the genome
+    int wf[VX_MAX_HIDDEN + 1], bias[VX_MAX_HIDDEN + 1];          // offsets in smem
+    int total_w;                                                 // weights + biases (doubles)
+    int rows;                                                    // activation rows (>= every padded width)
+};
+
+__device__ __forceinline__ void dmma884(double (&c)[2], double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(c[0]), "+d"(c[1])
+                 : "d"(a), "d"(b));
+}
+
+// One warp: output n-tile `nt`, m-tiles [mt0, mt1) of the 32-voxel tile.
+template <bool kTanh>
+__device__ __forceinline__ void mma_tile(const double* __restrict__ WF, const double* __restrict__ bias,
+                                         const double* __restrict__ X, double* __restrict__ Y, int KS, int nt,
+                                         int mt0, int mt1, int lane) {
+    double acc[kMmaMT][2];
+    const double b0 = bias[nt * 8 + 2 * (lane & 3)], b1 = bias[nt * 8 + 2 * (lane & 3) + 1];
+#pragma unroll
+    for (int mt = 0; mt < kMmaMT; ++mt) {
+        acc[mt][0] = b0;
+        acc[mt][1] = b1;
+    }
+    const double* wf = WF + static_cast<size_t>(nt) * KS * 32 + lane;
+    const double* xa = X + (lane & 3) * kXS + (lane >> 2);
+    for (int ks = 0; ks < KS; ++ks) {
+        const double b = wf[ks * 32];
+#pragma unroll
+        for (int mt = 0; mt < kMmaMT; ++mt)
+            if (mt >= mt0 && mt < mt1) dmma884(acc[mt], xa[ks * 4 * kXS + mt * 8], b);
+    }
+#pragma unroll
+    for (int mt = 0; mt < kMmaMT; ++mt) {
+        if (mt < mt0 || mt >= mt1) continue;
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+            const int n = nt * 8 + 2 * (lane & 3) + i;
+            Y[n * kXS + mt * 8 + (lane >> 2)] = kTanh ? tanh(acc[mt][i]) : acc[mt][i];
+        }
+    }
+}
+
+template <bool kTanh>
+__device__ __forceinline__ void mma_layer(const double* WF, const double* bias, const double* X, double* Y, int in,
+                                          int out, int wid, int lane) {
+    const int NT = (out + 7) / 8, KS = (in + 3) / 4;
+    if (NT >= kWarps) {
+        for (int nt = wid; nt < NT; nt += kWarps) mma_tile<kTanh>(WF, bias, X, Y, KS, nt, 0, kMmaMT, lane);
+    } else {
+        const int wpn = kWarps / NT;  // warps per n-tile split the m-tiles
+        if (wid < NT * wpn) {
+            const int nt = wid / wpn, part = wid % wpn;
+            const int mt0 = part * kMmaMT / wpn, mt1 = (part + 1) * kMmaMT / wpn;
+            if (mt0 < mt1) mma_tile<kTanh>(WF, bias, X, Y, KS, nt, mt0, mt1, lane);
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kThreads) decode_mma_kernel(DecodeArgs A, MmaLayout Lo, uint8_t* fix) {
+    const int g = A.select ? A.select[blockIdx.x] : static_cast<int>(blockIdx.x);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    double* sm = reinterpret_cast<double*>(smem_raw);
+    const double* gp = A.params + static_cast<size_t>(g) * A.np;
+    // weights in fragment order + padded biases
+    for (int l = 0; l < Lo.nl; ++l) {
+        const int in = Lo.in[l], out = Lo.out[l], KS = (in + 3) / 4, NT = (out + 7) / 8;
+        const bool head = l == Lo.nl - 1;
+        const int nfrag = NT * KS * 32;
+        double* wf = sm + Lo.wf[l];
+        for (int q = threadIdx.x; q < nfrag; q += kThreads) {
+            const int ln = q & 31, ks = (q >> 5) % KS, nt = (q >> 5) / KS;
+            const int n = nt * 8 + (ln >> 2), k = ks * 4 + (ln & 3);
+            double v = 0.0;
+            if (k < in && n < out) {
+                // head: material rows 0..4 (Wm) then the weight row (Ww, after bm)
+                const int64_t src = head && n == VX_NMAT ? Lo.src_w[l] + static_cast<int64_t>(VX_NMAT) * in + VX_NMAT + k
+                                                         : Lo.src_w[l] + static_cast<int64_t>(n) * in + k;
+                v = gp[src];
+            }
+            wf[q] = v;
+        }
+        double* bs = sm + Lo.bias[l];
+        for (int n = threadIdx.x; n < NT * 8; n += kThreads) {
+            double v = 0.0;
+            if (n < out) v = head && n == VX_NMAT ? gp[Lo.src_b[l] + VX_NMAT + in] : gp[Lo.src_b[l] + n];
+            bs[n] = v;
+        }
+    }
+    double* Bm = sm + Lo.total_w;  // 3m
+    double* X = Bm + 3 * A.m;      // [rows][kXS]
+    double* Y = X + Lo.rows * kXS;
+    double* L = Y + Lo.rows * kXS;  // logits [8][kXS]
+    for (int q = threadIdx.x; q < 3 * A.m; q += kThreads) Bm[q] = A.bmat[static_cast<size_t>(g) * 3 * A.m + q];
+    __syncthreads();
+
+    const int ncell = A.w * A.h * A.d;
+    const int m = A.m, in0 = 2 * m, in0p = ((in0 + 3) / 4) * 4;
+    bool need_fix = false;
+    for (int t0 = 0; t0 < ncell; t0 += kMmaTile) {
+        // gaussian_encode (genome.hpp:169-179) for 32 voxels; K padding zeroed
+        for (int q = threadIdx.x; q < m * kMmaTile; q += kThreads) {
+            const int r = q / kMmaTile, vx_ = q % kMmaTile, cell = t0 + vx_;
+            double sn = 0.0, cs = 0.0;
+            if (cell < ncell) {
+                const int x = cell % A.w, y = (cell / A.w) % A.h, z = cell / (A.w * A.h);
+                const double v0 = (x + 0.5) / A.w, v1 = (y + 0.5) / A.h, v2 = (z + 0.5) / A.d;  // morphology.hpp:147
+                const double phase = kTwoPi * (Bm[3 * r] * v0 + Bm[3 * r + 1] * v1 + Bm[3 * r + 2] * v2);
+                sincos(phase, &sn, &cs);
+            }
+            X[r * kXS + vx_] = cs;
+            X[(m + r) * kXS + vx_] = sn;
+        }
+        for (int q = threadIdx.x; q < (in0p - in0) * kMmaTile; q += kThreads)
+            X[(in0 + q / kMmaTile) * kXS + q % kMmaTile] = 0.0;
+        __syncthreads();
+        for (int l = 0; l + 1 < Lo.nl; ++l) {  // hidden: affine + tanh (genome.hpp:192)
+            mma_layer<true>(sm + Lo.wf[l], sm + Lo.bias[l], X, Y, Lo.in[l], Lo.out[l], wid, lane);
+            __syncthreads();
+            double* t = X;
+            X = Y;
+            Y = t;
+        }
+        mma_layer<false>(sm + Lo.wf[Lo.nl - 1], sm + Lo.bias[Lo.nl - 1], X, L, Lo.in[Lo.nl - 1], VX_NMAT + 1, wid,
+                         lane);
+        __syncthreads();
+        if (wid == 0 && t0 + lane < ncell) {
+            const int cell = t0 + lane;
+            double lg[VX_NMAT];
+            for (int i = 0; i < VX_NMAT; ++i) lg[i] = L[i * kXS + lane];
+            double mx = lg[0];  // std::max_element: first maximal
+            for (int i = 1; i < VX_NMAT; ++i)
+                if (mx < lg[i]) mx = lg[i];
+            double p[VX_NMAT];
+            double sum = 0.0;
+            for (int i = 0; i < VX_NMAT; ++i) {
+                p[i] = exp(lg[i] - mx);
+                sum += p[i];
+            }
+            for (int i = 0; i < VX_NMAT; ++i) p[i] /= sum;
+            int best = 0;
+            for (int i = 1; i < VX_NMAT; ++i)
+                if (p[i] > p[best]) best = i;
+            double second = -1.0;
+            for (int i = 0; i < VX_NMAT; ++i)
+                if (i != best && p[i] > second) second = p[i];
+            if (p[best] - second < kFixGap * p[best]) need_fix = true;
+            const size_t o = static_cast<size_t>(g) * ncell + cell;
+            const double wgt = stable_sigmoid(L[VX_NMAT * kXS + lane]);
+            A.mat[o] = static_cast<uint8_t>(best);
+            A.weight[o] = wgt < kMinVoxelWeight ? kMinVoxelWeight : (wgt > 1.0 ? 1.0 : wgt);  // morphology.hpp:154
+        }
+        __syncthreads();
+    }
+    if (wid == 0) {
+        need_fix = __any_sync(0xffffffffu, need_fix);
+        if (lane == 0) fix[blockIdx.x] = need_fix ? 1 : 0;
     }
 }
 
@@ -395,12 +586,62 @@ vx_status decode_feasible(vx_ctx* ctx, const vx_arch* a) {
     return VX_OK;
 }
 
+// Tensor-pipe layout of the default decode (decode_mma_kernel); false when the
+// architecture's weights do not fit shared memory next to the activations.
+static bool mma_layout(const vx_ctx* ctx, const vx_arch* a, MmaLayout& Lo, size_t& smem) {
+    Lo = MmaLayout{};
+    Lo.nl = a->n_hidden + 1;
+    int in = 2 * a->m, rows = ((2 * a->m + 3) / 4) * 4;
+    int64_t src = 0;
+    int off = 0;
+    for (int l = 0; l < Lo.nl; ++l) {
+        const bool head = l == a->n_hidden;
+        const int out = head ? VX_NMAT + 1 : a->hidden[l];
+        Lo.in[l] = in;
+        Lo.out[l] = out;
+        Lo.src_w[l] = src;
+        Lo.src_b[l] = src + static_cast<int64_t>(head ? VX_NMAT : out) * in;
+        const int NT = (out + 7) / 8, KS = (in + 3) / 4;
+        Lo.wf[l] = off;
+        off += NT * KS * 32;
+        Lo.bias[l] = off;
+        off += NT * 8;
+        if (!head) {
+            src += static_cast<int64_t>(in) * out + out;
+            rows = rows > NT * 8 ? rows : NT * 8;
+            in = out;
+        }
+    }
+    Lo.total_w = off;
+    Lo.rows = rows;
+    smem = (static_cast<size_t>(off) + 3ull * a->m + (2ull * rows + 8) * kXS) * sizeof(double);
+    return smem + 1024 <= ctx->smem_optin;
+}
+
 vx_status launch_decode(vx_ctx* ctx, const vx_arch* a, int64_t np, int maxw, DecodeArgs& A, int n) {
     const size_t act = (2ull * maxw + VX_NMAT + 1) * kTile * sizeof(double) + 3ull * a->m * sizeof(double);
     size_t smem = act + static_cast<size_t>(np) * sizeof(double);
     A.params_in_smem = smem + 1024 <= ctx->smem_optin;
     if (!A.params_in_smem) smem = act;
     if (smem > ctx->smem_optin) return (set_error("decode: architecture too wide"), VX_EINVAL);
+    // decode(): the MLP layers on the FP64 tensor pipe, exact re-decode of flagged
+    // genomes; forward() point queries and VX_DECODE=exact keep the CUDA-core kernel
+    MmaLayout Lo;
+    size_t smem_mma = 0;
+    const char* mode = std::getenv("VX_DECODE");
+    const bool exact = mode && std::strcmp(mode, "exact") == 0;
+    if (!A.points && !exact && mma_layout(ctx, a, Lo, smem_mma)) {
+        VX_TRY(ctx->decode_fix.alloc(static_cast<size_t>(n)));
+        VX_CUDA(cudaFuncSetAttribute(decode_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(smem_mma)));
+        decode_mma_kernel<<<n, kThreads, smem_mma, ctx->stream>>>(A, Lo, ctx->decode_fix.p);
+        ctx->launches++;
+        VX_CUDA(cudaGetLastError());
+        A.fix_only = ctx->decode_fix.p;
+        ctx->decode_fix_n = n;
+    } else {
+        ctx->decode_fix_n = -1;
+    }
     VX_CUDA(cudaFuncSetAttribute(decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     decode_kernel<<<n, kThreads, smem, ctx->stream>>>(A);
     ctx->launches++;
