@@ -212,6 +212,110 @@ def run_reference(args, W):
     print(json.dumps(line))
 
 
+def run_cpu_protocol(args):
+    """--cpu-protocol: BASELINE.md §3's CPU-baseline protocol, the reference
+    (oracle/_ref: its headers compiled -O2, no -march, -ffp-contract=off) on
+    this box's host cores, with the GPU's run_bench beside it.  Bounded: every
+    CPU measurement is a few seconds of work; configs 3-5 and the O(P^2)
+    diversity are measured at a reduced population and extrapolated (labelled).
+    Prints one JSON object."""
+    import oracle
+    if not oracle.have_reference():
+        print(json.dumps({"cpu_protocol": "unavailable", "why": "oracle/_ref/libvoxevo_ref.so not built"}))
+        return
+    ref = oracle.reference()
+    cores = os.cpu_count() or 1
+    out = {"cpu_protocol": "BASELINE.md §3", "host": host_info(),
+           "build": "reference headers, g++ -std=c++20 -O2 -ffp-contract=off, no -march (oracle/Makefile)",
+           "libm": "default glibc ifunc selection (no GLIBC_TUNABLES)"}
+    # 1. run_bench (bench.hpp:50-86) on bench_robot(n), 1 thread and all cores
+    rb = []
+    for n in (4, 6, 10, 20):
+        springs = None
+        for threads in (1, cores):
+            jobs = 2 if threads == 1 else 2 * threads
+            probe = np.zeros(6)
+            ref._run_bench(1, 1, 1, n, DT, probe.ctypes.data)
+            springs = int(probe[0])
+            target = 1.5e8 * (1 if threads == 1 else max(1, threads // 2))  # ~2-4 s of CPU work
+            steps = max(50, int(target / (jobs * springs)))
+            o = np.zeros(6)
+            ref._run_bench(jobs, steps, threads, n, DT, o.ctypes.data)
+            assert int(o[1]) == int(o[2]), "run_bench audit mismatch"
+            rb.append({"n": n, "threads": threads, "jobs": jobs, "steps": steps, "springs_per_robot": springs,
+                       "spring_updates": int(o[1]), "seconds": o[3], "updates_per_s": o[4]})
+    out["run_bench"] = rb
+    # the same harness on the B200 (vx_run_bench: one batched launch)
+    try:
+        import paper_2405_00698_b200 as vx
+        ctx = vx.Context(0)
+        gb = []
+        for n in (4, 6, 10, 20):
+            jobs, steps = (296, 5000) if n <= 10 else (148, 500)
+            vx.run_bench(jobs=jobs, steps=50, grid=n, ctx=ctx)  # warm-up
+            r = vx.run_bench(jobs=jobs, steps=steps, grid=n, ctx=ctx)
+            assert r["spring_updates"] == r["expected_updates"]
+            gb.append({"n": n, "jobs": jobs, "steps": steps, "spring_updates": r["spring_updates"],
+                       "seconds": r["seconds"], "updates_per_s": r["updates_per_second"]})
+        out["run_bench_b200"] = gb
+    except Exception as e:  # CPU-only host: the reference half still stands
+        out["run_bench_b200"] = f"unavailable: {e}"
+    sim = oracle.sim6(dt=DT, duration=SIM_STEPS * DT)
+    # 2. config 1: one 4^3 robot from sample_genome({32,3,1.0},{64,64},seed), 1000 steps
+    sim1 = oracle.sim6(dt=DT, duration=1000 * DT)
+    p1, b1 = ref.sample_genome(32, [64, 64], SEED)
+    t0 = time.perf_counter()
+    m1, w1 = ref.decode(32, [64, 64], p1, b1, 4, 4, 4)
+    f1 = ref.evaluate_fitness(m1, w1, 4, 4, 4, sim=sim1)
+    out["config1"] = {"seconds": time.perf_counter() - t0, "fitness": f1,
+                      "what": "decode + evaluate_fitness of one 4^3 robot, 1000 steps, 1 thread"}
+    # 3./4./6. configs 2-5: evolve_generation wall (generations/s), reduced P for 3-5 (extrapolated)
+    gens = []
+    for name, P_full, P, g in (("config2", 256, 256, 6), ("config3", 4096, 64, 10), ("config4", 65536, 64, 10),
+                               ("config5", 1024, 8, 20)):
+        if name == "config4":  # same robots as config 3 at 16x the population: extrapolate config 3's sample
+            c3 = gens[-1]
+            gens.append({"config": name, "P": P_full, "extrapolated_from": "config3 sample",
+                         "seconds_per_generation": c3["seconds_per_generation"] * P_full / 4096,
+                         "generations_per_s": 1.0 / (c3["seconds_per_generation"] * P_full / 4096),
+                         "updates_per_s": c3["updates_per_s"]})
+            continue
+        ev = ref.evo(population=P, generations=0, grid=(g, g, g), seed=SEED, threads=cores, sim=sim)
+        _, secs, upd = ev.generation_timed()  # generation 0: every robot evaluated
+        row = {"config": name, "P": P_full, "P_measured": P, "threads": cores, "seconds_measured": secs,
+               "generation": "0 (every robot evaluated; later generations evaluate ~0.7P)",
+               "spring_updates_measured": int(upd), "updates_per_s": upd / secs}
+        row["seconds_per_generation"] = secs * P_full / P
+        row["generations_per_s"] = 1.0 / row["seconds_per_generation"]
+        if P != P_full:
+            row["extrapolated"] = f"linear in P from a P={P} generation 0 (exact update count)"
+        gens.append(row)
+    out["evolve_generation"] = gens
+    # 5. serial stages: decode (morphology.hpp:141) and population_diversity (evolution.hpp:89)
+    dec = []
+    for g in (4, 6, 10, 20):
+        reps = 8 if g <= 10 else 2
+        t0 = time.perf_counter()
+        for r in range(reps):
+            ref.decode(32, [64, 64], p1, b1, g, g, g)
+        dec.append({"grid": g, "seconds_per_genome": (time.perf_counter() - t0) / reps})
+    out["serial_decode"] = dec
+    div = []
+    rng = np.random.default_rng(0)
+    for name, P_full, P, g in (("config2", 256, 256, 6), ("config3", 4096, 512, 10), ("config5", 1024, 128, 20)):
+        mats = rng.integers(0, 5, (P, g ** 3), dtype=np.uint8)
+        t0 = time.perf_counter()
+        ref.population_diversity(mats)
+        secs = time.perf_counter() - t0
+        row = {"config": name, "P": P_full, "P_measured": P, "seconds_measured": secs,
+               "seconds_at_P": secs * (P_full / P) ** 2}
+        if P != P_full:
+            row["extrapolated"] = "quadratic in P (O(P^2 cells) pair loop)"
+        div.append(row)
+    out["serial_diversity"] = div
+    print(json.dumps(out))
+
+
 def cpu_baseline_and_parity(W, params0, bmat0, fit0_gpu):
     """The reference (oracle/_ref) on a bounded sample of this run's generation-0
     robots: its own decode, then evaluate_fitness through its parallel_for on
@@ -268,7 +372,12 @@ def main():
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer e2e leg (profiling runs)")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no baselines, no clocks)")
     ap.add_argument("--workload", default="config3", choices=sorted(WORKLOADS))
+    ap.add_argument("--cpu-protocol", action="store_true",
+                    help="BASELINE.md §3: the reference's CPU protocol on this host (+ GPU run_bench beside it)")
     args = ap.parse_args()
+    if args.cpu_protocol:
+        run_cpu_protocol(args)
+        return
     W = WORKLOADS[args.workload]
     rank, world, local = rank_info()
     launched = "RANK" in os.environ and "MASTER_ADDR" in os.environ
