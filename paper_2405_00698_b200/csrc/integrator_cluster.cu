@@ -665,8 +665,13 @@ __device__ __forceinline__ void cluster_vertex_robot(const ClArgs& A, const int 
         com_start[1] = c1;
         com_start[2] = c2;
     }
+#ifdef VX_CL_ASM_REMOTE
     const uint32_t f_prev = rank > 0 ? map_rank(smem_addr(F), rank - 1) : 0u;
     const uint32_t x_next = has_next ? map_rank(smem_addr(X), rank + 1) : 0u;
+#else
+    double* const Fprev = map_generic(F, rank > 0 ? rank - 1 : 0u);
+    double* const Xnext = map_generic(X, has_next ? rank + 1 : rank);
+#endif
     const uint32_t flag_local = smem_addr(&s_flag);
     cluster_barrier();  // every CTA initialised (MAP and staging in F are dead) before any remote store
 
@@ -698,11 +703,16 @@ __device__ __forceinline__ void cluster_vertex_robot(const ClArgs& A, const int 
                     double dy = x1 - Xa[XS - off];
                     double dz = x2 - Xa[2 * XS - off];
                     const double len2 = dx * dx + dy * dy + dz * dz;
+#ifdef VX_CL_SPLIT_SQRT
                     const double len = sqrt_rn_fast(len2);
+                    const double inv_len = rcp_rn_fast(len);
+#else
+                    double len, inv_len;  // RN(sqrt) and RN(1/len) from one refined rsqrt
+                    sqrt_rcp_rn_fast(len2, len, inv_len);
+#endif
                     zero_len |= (valid && len2 < A.zero_len2) ? 1 : 0;
                     const double r0 = PR[d * kNmp + a];
                     const double rest = r0 + (SA[vox] * r0) * D[vox];
-                    const double inv_len = rcp_rn_fast(len);
                     const double nx = dx * inv_len, ny = dy * inv_len, nz = dz * inv_len;
                     const double rel = (v0 - Xa[3 * XS - off]) * nx + (v1 - Xa[4 * XS - off]) * ny +
                                        (v2 - Xa[5 * XS - off]) * nz;
@@ -728,10 +738,19 @@ __device__ __forceinline__ void cluster_vertex_robot(const ClArgs& A, const int 
                         F[(3 * d + 1) * kNmp + li] = ofy[qq];
                         F[(3 * d + 2) * kNmp + li] = ofz[qq];
                     }
+#ifdef VX_CL_ASM_REMOTE
                     const uint32_t o = f_prev + 8u * static_cast<uint32_t>((3 * d) * kNmp + li + Q);
                     st_remote_if(valid && rem, o, ofx[qq]);
                     st_remote_if(valid && rem, o + 8u * kNmp, ofy[qq]);
                     st_remote_if(valid && rem, o + 16u * kNmp, ofz[qq]);
+#else
+                    if (valid && rem) {  // lower endpoint in the previous CTA: its slot, over DSMEM
+                        double* o = Fprev + (3 * d) * kNmp + li + Q;
+                        o[0] = ofx[qq];
+                        o[kNmp] = ofy[qq];
+                        o[2 * kNmp] = ofz[qq];
+                    }
+#endif
                 }
             };
             // chunks 12..9 | 8..4 | 3..0, each skipped when no lane of the warp
@@ -795,6 +814,7 @@ __device__ __forceinline__ void cluster_vertex_robot(const ClArgs& A, const int 
             X[4 * XS + PAD + a] = v1;
             X[5 * XS + PAD + a] = v2;
             if (push_halo) {  // the next CTA's halo copy of this key: row a - Q + PAD there
+#ifdef VX_CL_ASM_REMOTE
                 const uint32_t o = x_next + 8u * static_cast<uint32_t>(a - Q + PAD);
                 st_remote(o, x0);
                 st_remote(o + 8u * XS, x1);
@@ -802,6 +822,15 @@ __device__ __forceinline__ void cluster_vertex_robot(const ClArgs& A, const int 
                 st_remote(o + 24u * XS, v0);
                 st_remote(o + 32u * XS, v1);
                 st_remote(o + 40u * XS, v2);
+#else
+                double* o = Xnext + (a - Q + PAD);
+                o[0] = x0;
+                o[XS] = x1;
+                o[2 * XS] = x2;
+                o[3 * XS] = v0;
+                o[4 * XS] = v1;
+                o[5 * XS] = v2;
+#endif
             }
             const double speed_sq = v0 * v0 + v1 * v1 + v2 * v2;
             if (speed_sq > max_sq) max_sq = speed_sq;

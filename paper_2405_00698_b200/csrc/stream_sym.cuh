@@ -350,10 +350,15 @@ __device__ void sym_robot(const SymArgs& A, int r, unsigned char* base) {
                 const double dy = Xj[XS] - xi1;
                 const double dz = Xj[2 * XS] - xi2;
                 const double len2 = dx * dx + dy * dy + dz * dz;
+#ifdef VX_SYM_SPLIT_SQRT
                 const double len = sqrt_rn_fast(len2);
+                const double inv_len = rcp_rn_fast(len);
+#else
+                double len, inv_len;  // RN(sqrt) and RN(1/len) from one refined rsqrt
+                sqrt_rcp_rn_fast(len2, len, inv_len);
+#endif
                 zero_len |= (valid && len2 < A.zero_len2) ? 1 : 0;
                 const double rest = r0 + (SA[vox] * r0) * Dc[vox];
-                const double inv_len = rcp_rn_fast(len);
                 const double nx = dx * inv_len, ny = dy * inv_len, nz = dz * inv_len;
                 const double rel = (Xj[3 * XS] - vi0) * nx + (Xj[4 * XS] - vi1) * ny + (Xj[5 * XS] - vi2) * nz;
                 const double cc = A.zeta2 * sqrt_rn_fast(kk * A.mu);  // damping_coefficient (physics.hpp:66-71)

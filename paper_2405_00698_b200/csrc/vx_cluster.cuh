@@ -16,6 +16,16 @@ __device__ __forceinline__ uint32_t map_rank(uint32_t addr, uint32_t rank) {
     asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
     return r;
 }
+// generic address of the same shared-memory object in CTA `rank` of the
+// cluster: stores through it are plain (predicable, schedulable) generic
+// stores with the 64-bit base computed once, instead of a shared::cluster
+// store that ptxas rebuilds from the shared window every time
+template <typename T>
+__device__ __forceinline__ T* map_generic(T* p, uint32_t rank) {
+    uint64_t r;
+    asm("mapa.u64 %0, %1, %2;" : "=l"(r) : "l"(reinterpret_cast<uint64_t>(p)), "r"(rank));
+    return reinterpret_cast<T*>(r);
+}
 __device__ __forceinline__ void st_remote(uint32_t addr, double v) {
     asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(addr), "d"(v));
 }
