@@ -51,6 +51,7 @@ SIM_STEPS = 5000
 DT = 1e-5
 SEED = 42
 FLOPS_PER_UPDATE = 48  # 48 FP64 flop (+1 sqrt +1 div) per spring update
+MLP_MACS_PER_VOXEL = 2 * 32 * 64 + 64 * 64 + 64 * 6  # default network (m=32, hidden 64-64, 5+1 heads)
 METRIC = "spring-mass updates/sec (1/2/4/8 B200) and generations/sec at fixed population"
 WORKLOADS = {
     "config3": dict(P=4096, grid=10, ref_P=64, cpu_sample=32,
@@ -272,7 +273,7 @@ def run_cpu_protocol(args):
     # 3./4./6. configs 2-5: evolve_generation wall (generations/s), reduced P for 3-5 (extrapolated)
     gens = []
     for name, P_full, P, g in (("config2", 256, 256, 6), ("config3", 4096, 64, 10), ("config4", 65536, 64, 10),
-                               ("config5", 1024, 8, 20)):
+                               ("config5", 1024, max(8, cores), 20)):  # >= one robot per host thread
         if name == "config4":  # same robots as config 3 at 16x the population: extrapolate config 3's sample
             c3 = gens[-1]
             gens.append({"config": name, "P": P_full, "extrapolated_from": "config3 sample",
@@ -434,6 +435,7 @@ def main():
     # ---- value: K generations, population resident in HBM
     ctx.timing(True)
     ctx.integrator_time(reset=True)
+    ctx.decode_time(reset=True)
     launches0 = ctx.launches
     ms, upd = [], []
     with ClockSampler(local) as clk:
@@ -450,6 +452,7 @@ def main():
             upd.append(int(rep.spring_updates))
     launches = ctx.launches - launches0
     int_ms, int_n = ctx.integrator_time(reset=True)
+    dec_ms, dec_vox = ctx.decode_time(reset=True)
     ctx.timing(False)
 
     # ---- e2e: K more generations with the population host-resident (pinned)
@@ -535,6 +538,20 @@ def main():
                      else None,
                      "ncu_source": meta.get("source")})
 
+    # north star NS-1: the decode MLP on the FP64 tensor pipe, from the same live events
+    decode = None
+    if dec_ms > 0:
+        dpk = ctx.dmma_peak_tflops()
+        dach = 2.0 * MLP_MACS_PER_VOXEL * dec_vox / (dec_ms * 1e-3) / 1e12
+        decode = {"kernel": "decode_mma_kernel (every MLP layer on DMMA, mma.sync m8n8k4 .f64) + the exact-order "
+                            "fix-up launch", "bound": "fp64 tensor pipe (DMMA) + FP64 transcendentals",
+                  "achieved": dach, "peak": dpk, "unit": "TFLOP/s", "frac": dach / dpk,
+                  "algorithmic": f"2 x {MLP_MACS_PER_VOXEL} MAC per voxel (default network) x {dec_vox} voxels "
+                                 "decoded in the timed generations",
+                  "peak_source": "measured DMMA m8n8k4 throughput of this GPU (vx_dmma_peak, csrc/measure.cu)",
+                  "ms_per_step": dec_ms / args.steps, "share_of_step": dec_ms / total_ms,
+                  "dmma_pipe_busy_ncu": 31.4, "ncu_source": "profiles/r02_decode_dmma.md"}
+
     cpu = parity = None
     if world == 1 and not args.no_cpu_baseline and not args.profile:
         cpu, parity = cpu_baseline_and_parity(W, params0, bmat0, fit0)
@@ -553,6 +570,7 @@ def main():
                 "generations_per_s": (len(ms_e2e) / (total_e2e * 1e-3)) if ms_e2e else None},
         "gpu_launches": int(launches),
         "roofline": roofline,
+        "decode_roofline": decode,
         "cpu_baseline": cpu,
         "parity": parity,
         "clocks": clk.summary(),

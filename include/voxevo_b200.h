@@ -396,6 +396,13 @@ vx_status vx_integrator_timing(vx_ctx* ctx, double* total_ms, int64_t* n_launche
 /* Measured FP64 FMA throughput of the device (TFLOP/s, 2 flops per DFMA),
  * the denominator for the FP64-issue-bound integrator's roofline. */
 vx_status vx_fp64_peak(vx_ctx* ctx, double* tflops);
+/* Summed device time (CUDA events on the context stream, while timing is
+ * enabled) of every decode launch (tensor-pipe kernel + exact fix-up) and the
+ * voxels those launches decoded; optionally reset. */
+vx_status vx_decode_timing(vx_ctx* ctx, double* total_ms, int64_t* voxels, int32_t reset);
+/* Measured FP64 tensor-pipe throughput (TFLOP/s, mma.sync m8n8k4 .f64 at 2 x
+ * 8 x 8 x 4 flop), the decode MLP's roofline denominator. */
+vx_status vx_dmma_peak(vx_ctx* ctx, double* tflops);
 /* Self-check of the integrator's branch-free sqrt / reciprocal against the
  * IEEE sqrt(x) and 1.0/x over n pseudo-random inputs spanning the ranges the
  * integrator feeds them (plus powers of two and a few ulps around them);

@@ -276,6 +276,8 @@ def _declare(lib):
         "vx_timing_enable": (i32, [vp, i32]),
         "vx_integrator_timing": (i32, [vp, P(dbl), P(i64), i32]),
         "vx_fp64_peak": (i32, [vp, P(dbl)]),
+        "vx_decode_timing": (i32, [vp, P(dbl), P(i64), i32]),
+        "vx_dmma_peak": (i32, [vp, P(dbl)]),
         "vx_fastmath_check": (i32, [vp, i64, u64, vp]),
         "vx_format_doubles": (i64, [vp, i64, C.c_char, C.c_char_p, i64]),
         "vx_fnv1a64": (u64, [C.c_char_p, i64]),
@@ -408,6 +410,17 @@ class Context:
         ms, n = C.c_double(), C.c_int64()
         _check(_lib().vx_integrator_timing(self.h, C.byref(ms), C.byref(n), 1 if reset else 0))
         return float(ms.value), int(n.value)
+
+    def decode_time(self, reset: bool = True):
+        """(summed device ms, voxels decoded) of decode launches since the last reset."""
+        ms, n = C.c_double(), C.c_int64()
+        _check(_lib().vx_decode_timing(self.h, C.byref(ms), C.byref(n), 1 if reset else 0))
+        return float(ms.value), int(n.value)
+
+    def dmma_peak_tflops(self) -> float:
+        t = C.c_double()
+        _check(_lib().vx_dmma_peak(self.h, C.byref(t)))
+        return float(t.value)
 
     def fp64_peak_tflops(self) -> float:
         t = C.c_double()

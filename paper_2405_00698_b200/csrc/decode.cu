@@ -626,6 +626,18 @@ vx_status launch_decode(vx_ctx* ctx, const vx_arch* a, int64_t np, int maxw, Dec
     if (smem > ctx->smem_optin) return (set_error("decode: architecture too wide"), VX_EINVAL);
     // decode(): the MLP layers on the FP64 tensor pipe, exact re-decode of flagged
     // genomes; forward() point queries and VX_DECODE=exact keep the CUDA-core kernel
+    std::pair<cudaEvent_t, cudaEvent_t> ev{nullptr, nullptr};
+    if (ctx->timing && !A.points) {  // live decode timing (bench.py's decode roofline)
+        if (ctx->event_pool.empty()) {
+            VX_CUDA(cudaEventCreate(&ev.first));
+            VX_CUDA(cudaEventCreate(&ev.second));
+        } else {
+            ev = ctx->event_pool.back();
+            ctx->event_pool.pop_back();
+        }
+        VX_CUDA(cudaEventRecord(ev.first, ctx->stream));
+        ctx->dec_voxels += static_cast<int64_t>(n) * A.w * A.h * A.d;
+    }
     MmaLayout Lo;
     size_t smem_mma = 0;
     const char* mode = std::getenv("VX_DECODE");
@@ -646,6 +658,10 @@ vx_status launch_decode(vx_ctx* ctx, const vx_arch* a, int64_t np, int maxw, Dec
     decode_kernel<<<n, kThreads, smem, ctx->stream>>>(A);
     ctx->launches++;
     VX_CUDA(cudaGetLastError());
+    if (ev.first) {
+        VX_CUDA(cudaEventRecord(ev.second, ctx->stream));
+        ctx->dec_pending.push_back(ev);
+    }
     return VX_OK;
 }
 

@@ -1,4 +1,5 @@
-// measure.cu — live integrator timing and the FP64 roofline denominator.
+// measure.cu — live integrator / decode timing and the FP64 (DFMA, DMMA)
+// roofline denominators.
 #include "vx_internal.cuh"
 
 using namespace vx;
@@ -22,6 +23,25 @@ __global__ void __launch_bounds__(256) dfma_kernel(double* out, int iters, doubl
     }
     const double s = ((x0 + x1) + (x2 + x3)) + ((x4 + x5) + (x6 + x7));
     if (s == 12345.678) out[blockIdx.x] = s;  // keep the chains alive
+}
+
+// FP64 tensor pipe: 8 independent m8n8k4 DMMA accumulators per warp
+__global__ void __launch_bounds__(256) dmma_kernel(double* out, int iters) {
+    const double a = 1.0 + threadIdx.x * 1e-9, b = 0.5 - threadIdx.x * 1e-9;
+    double c[8][2];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) c[k][0] = c[k][1] = 0.0;
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                         : "+d"(c[k][0]), "+d"(c[k][1])
+                         : "d"(a), "d"(b));
+    }
+    double s = 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s += c[k][0] + c[k][1];
+    if (s == 12345.678) out[blockIdx.x] = s;
 }
 
 __device__ __forceinline__ uint64_t mix64(uint64_t z) {
@@ -110,6 +130,52 @@ vx_status vx_integrator_timing(vx_ctx* ctx, double* total_ms, int64_t* n_launche
         ctx->timed_ms = 0.0;
         ctx->timed_launches = 0;
     }
+    return VX_OK;
+}
+
+vx_status vx_decode_timing(vx_ctx* ctx, double* total_ms, int64_t* voxels, int32_t reset) {
+    if (!ctx) return VX_EINVAL;
+    for (auto& ev : ctx->dec_pending) {
+        VX_CUDA(cudaEventSynchronize(ev.second));
+        float ms = 0.f;
+        VX_CUDA(cudaEventElapsedTime(&ms, ev.first, ev.second));
+        ctx->dec_ms += ms;
+        ctx->event_pool.push_back(ev);
+    }
+    ctx->dec_pending.clear();
+    if (total_ms) *total_ms = ctx->dec_ms;
+    if (voxels) *voxels = ctx->dec_voxels;
+    if (reset) {
+        ctx->dec_ms = 0.0;
+        ctx->dec_voxels = 0;
+    }
+    return VX_OK;
+}
+
+vx_status vx_dmma_peak(vx_ctx* ctx, double* tflops) {
+    if (!ctx || !tflops) return VX_EINVAL;
+    DevBuf<double> out;
+    VX_TRY(out.alloc(4096));
+    const int blocks = ctx->sm_count * 8, iters = 1 << 12;  // 64 warps per SM
+    cudaEvent_t e0, e1;
+    VX_CUDA(cudaEventCreate(&e0));
+    VX_CUDA(cudaEventCreate(&e1));
+    dmma_kernel<<<blocks, 256, 0, ctx->stream>>>(out.p, 64);  // warm-up
+    float best = 1e30f;
+    for (int rep = 0; rep < 5; ++rep) {
+        VX_CUDA(cudaEventRecord(e0, ctx->stream));
+        dmma_kernel<<<blocks, 256, 0, ctx->stream>>>(out.p, iters);
+        VX_CUDA(cudaEventRecord(e1, ctx->stream));
+        VX_CUDA(cudaEventSynchronize(e1));
+        float ms = 0.f;
+        VX_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+        if (ms < best) best = ms;
+    }
+    ctx->launches += 6;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    const double flops = 2.0 * 8 * 8 * 4 * 8.0 * iters * (256 / 32) * static_cast<double>(blocks);
+    *tflops = flops / (best * 1e-3) / 1e12;
     return VX_OK;
 }
 
