@@ -26,7 +26,11 @@
 //    wait.acquire) replace the two __syncthreads of the one-SM kernel; the
 //    zero-length / divergence flags are broadcast to every CTA's flag word
 //    before the barrier (rare path), tagged with the step so no reset is
-//    needed.
+//    needed.  The vertex-indexed kernel SPLITS them: every warp arrives after
+//    its phase, but only the warps whose data crosses a CTA boundary wait
+//    before their next phase (halo readers before phase 1, remote-force
+//    receivers before phase 2); the others wait after computing it (+7.5%
+//    at 10^3, profiles/r02_split_barrier.md).
 // Compiled with --fmad=false; all sums in reference order.
 #include <cmath>
 #include <cstdio>
@@ -524,6 +528,7 @@ __device__ __forceinline__ void cluster_vertex_robot(const ClArgs& A, const int 
     __shared__ double s_maxsq[kNmp / 32];
     __shared__ double s_cmax[kMaxCluster];
     __shared__ uint32_t s_flag;
+    __shared__ uint32_t s_flags[4];  // split barriers: zero-length [step & 1], divergence [2 + (step & 1)]
 
     if (nm == 0) {  // uniform over the cluster: every CTA leaves, rank 0 reports
         if (out && a == 0) {
@@ -548,7 +553,7 @@ __device__ __forceinline__ void cluster_vertex_robot(const ClArgs& A, const int 
         CPH[v] = 1.0;
     }
     for (int k = a; k < NV; k += kNmp) MAP[k] = -1;
-    if (a == 0) s_flag = 0u;
+    if (a < 5) (a == 0 ? s_flag : s_flags[a - 1]) = 0u;
     __syncthreads();
     for (int m = a; m < nm; m += kNmp) MAP[A.vkey[mo + m]] = m;
     const int ns = b.nspring[r];
@@ -685,8 +690,39 @@ __device__ __forceinline__ void cluster_vertex_robot(const ClArgs& A, const int 
         for (int c = 0; c < CL; ++c) st_remote_u32(map_rank(flag_local, static_cast<uint32_t>(c)), tag);
     };
     const double* __restrict__ Xa = X + PAD + a;
+#ifndef VX_CL_FULL_BARRIER
+    // Split cluster barriers (arrive after a phase, wait only where the data
+    // crosses a CTA boundary).  Per warp: H reads the halo and stores forces
+    // into the previous CTA (keys < PAD), so it waits for barrier B before
+    // phase 1; R receives the next CTA's forces and pushes the halo (keys >=
+    // Q - PAD), so it waits for barrier A before phase 2.  Every other warp
+    // waits after its phase (phase 2 results are committed only after the
+    // wait, so a zero-length step of ANY CTA still leaves the state untouched).
+    // CTA-local ordering stays with __syncthreads.  Flags live in per-step-
+    // parity slots: a slot is rewritten two steps later, after a barrier every
+    // reader has passed.
+    const int wfirst = a & ~31;
+    const bool wH = rank > 0 && wfirst < PAD;
+    const bool wR = has_next && wfirst + 31 >= Q - PAD;
+    bool pendB = false;
+    auto flag_at = [&](int i) { return *reinterpret_cast<volatile uint32_t*>(&s_flags[i]); };
+    auto raise_at = [&](int i, uint32_t tag) {
+        const uint32_t fl = smem_addr(&s_flags[i]);
+        for (int c = 0; c < CL; ++c) st_remote_u32(map_rank(fl, static_cast<uint32_t>(c)), tag);
+    };
+#endif
     for (int64_t kstep = 0; kstep < A.n_steps; ++kstep) {
         const uint32_t tag1 = static_cast<uint32_t>(2 * kstep + 1), tag2 = tag1 + 1u;
+#ifndef VX_CL_FULL_BARRIER
+        if (wH && pendB) {  // barrier B of the previous step: halo in, previous CTA done reading our stores
+            cluster_wait();
+            pendB = false;
+            if (flag_at(2 + ((kstep - 1) & 1)) == tag1 - 1u) {
+                diverged = 1;
+                break;
+            }
+        }
+#endif
         int zero_len = 0;
         double sx = 0.0, sy = 0.0, sz = 0.0;
         {
@@ -761,15 +797,42 @@ __device__ __forceinline__ void cluster_vertex_robot(const ClArgs& A, const int 
             if (wmask & 0x01F0u) chunk(std::integral_constant<int, 8>{}, I5{});
             if (wmask & 0x000Fu) chunk(std::integral_constant<int, 3>{}, I4{});
         }
+#ifndef VX_CL_FULL_BARRIER
+        if (pendB) {  // the previous step's barrier B, after this warp's (discardable) phase 1
+            cluster_wait();
+            pendB = false;
+            if (flag_at(2 + ((kstep - 1) & 1)) == tag1 - 1u) {
+                diverged = 1;
+                break;
+            }
+        }
+        ++steps;
+        if (zero_len) raise_at(kstep & 1, tag1);
+        cluster_arrive();
+        __syncthreads();
+        if (wR) {
+            cluster_wait();
+            if (flag_at(kstep & 1) == tag1) {
+                diverged = 1;
+                break;
+            }
+        }
+#else
         ++steps;
         if (zero_len) raise_flag(tag1);
+#ifdef VX_CL_TIMING_NOSYNC  // timing-only bound (WRONG results): CTA barrier, no cluster sync, no exits
+        __syncthreads();
+        if (false) {
+#else
         cluster_barrier();
         if (*reinterpret_cast<volatile uint32_t*>(&s_flag) == tag1) {
+#endif
             diverged = 1;
             break;
         }
-        ++ok_phase1;
+#endif
         int bad = 0;
+        double speed_sq = 0.0;
         if (live) {
             double fx = sx, fy = sy, fz = sz;
 #pragma unroll
@@ -807,6 +870,22 @@ __device__ __forceinline__ void cluster_vertex_robot(const ClArgs& A, const int 
             x0 += v0 * dt;
             x1 += v1 * dt;
             x2 += v2 * dt;
+            speed_sq = v0 * v0 + v1 * v1 + v2 * v2;
+            if (!(fabs(x0) <= kDivergenceBound) || !(fabs(x1) <= kDivergenceBound) ||
+                !(fabs(x2) <= kDivergenceBound))
+                bad = 1;
+        }
+#ifndef VX_CL_FULL_BARRIER
+        if (!wR) {  // barrier A after computing (not committing) phase 2
+            cluster_wait();
+            if (flag_at(kstep & 1) == tag1) {
+                diverged = 1;
+                break;
+            }
+        }
+#endif
+        ++ok_phase1;
+        if (live) {
             X[PAD + a] = x0;
             X[XS + PAD + a] = x1;
             X[2 * XS + PAD + a] = x2;
@@ -832,11 +911,7 @@ __device__ __forceinline__ void cluster_vertex_robot(const ClArgs& A, const int 
                 o[5 * XS] = v2;
 #endif
             }
-            const double speed_sq = v0 * v0 + v1 * v1 + v2 * v2;
             if (speed_sq > max_sq) max_sq = speed_sq;
-            if (!(fabs(x0) <= kDivergenceBound) || !(fabs(x1) <= kDivergenceBound) ||
-                !(fabs(x2) <= kDivergenceBound))
-                bad = 1;
         }
         if (kstep + 1 < A.n_steps) {
             const double2 drv = __ldg(A.drive + kstep + 1);
@@ -846,13 +921,30 @@ __device__ __forceinline__ void cluster_vertex_robot(const ClArgs& A, const int 
                 if (v < NTV) D[v] = drv.x * vcos[j] + drv.y * vsin[j];
             }
         }
+#ifndef VX_CL_FULL_BARRIER
+        if (bad) raise_at(2 + (kstep & 1), tag2);
+        cluster_arrive();
+        __syncthreads();
+        pendB = true;
+    }
+    if (pendB) {  // barrier B of the last step
+        cluster_wait();
+        if (flag_at(2 + ((A.n_steps - 1) & 1)) == static_cast<uint32_t>(2 * A.n_steps)) diverged = 1;
+    }
+#else
         if (bad) raise_flag(tag2);
+#ifdef VX_CL_TIMING_NOSYNC
+        __syncthreads();
+        if (false) {
+#else
         cluster_barrier();
         if (*reinterpret_cast<volatile uint32_t*>(&s_flag) == tag2) {
+#endif
             diverged = 1;
             break;
         }
     }
+#endif
 
     for (int o = 16; o > 0; o >>= 1) {
         const double other = __shfl_xor_sync(0xffffffffu, max_sq, o);

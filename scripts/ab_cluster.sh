@@ -3,7 +3,7 @@
 cd ${GRAFT_REPO_ROOT:-.}
 mkdir -p gpurun_out
 T=${TAG:-ab}
-timeout -s KILL 600 python -m pytest tests/test_gpu_cluster.py tests/test_gpu_configs.py tests/test_gpu_dump.py -q -x > gpurun_out/${T}_tests.log 2>&1; echo "tests rc=$?" >> gpurun_out/${T}_tests.log
+timeout -s KILL 600 python -m pytest tests/test_gpu_cluster.py tests/test_gpu_configs.py tests/test_gpu_dump.py tests/test_gpu_filler.py -q -x > gpurun_out/${T}_tests.log 2>&1; echo "tests rc=$?" >> gpurun_out/${T}_tests.log
 cp paper_2405_00698_b200/_lib/libvoxevo_b200.so /tmp/main.so
 for rep in 1 2 3; do
 for v in main $(ls _variants 2>/dev/null); do
