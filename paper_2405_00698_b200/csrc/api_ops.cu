@@ -208,11 +208,12 @@ vx_status vx_diversity_from_histogram_dev(vx_ctx* ctx, int32_t P, int32_t cells,
 
 vx_status vx_population_diversity_dev(vx_ctx* ctx, int32_t P, int32_t cells, const uint8_t* d_mat, double* d_out) {
     if (!ctx || P < 0 || cells < 0) return VX_EINVAL;
-    DevBuf<int64_t> hist;
-    VX_TRY(hist.alloc(static_cast<size_t>(cells) * VX_NMAT + 1));
-    VX_TRY(histogram_dev(ctx, P, cells, d_mat, hist.p, false));
-    VX_TRY(diversity_from_hist_dev(ctx, P, cells, hist.p, d_out));
-    VX_CUDA(cudaStreamSynchronize(ctx->stream));  // hist is freed on return
+    // bit-exact: the reference's ordered pairwise sum (diversity.cu)
+    DevBuf<double> packed;
+    VX_TRY(packed.alloc(static_cast<size_t>(P) * diversity_words(cells) + 1));
+    VX_TRY(diversity_pack_dev(ctx, P, nullptr, cells, d_mat, packed.p));
+    VX_TRY(diversity_exact_dev(ctx, P, cells, packed.p, nullptr, d_out));
+    VX_CUDA(cudaStreamSynchronize(ctx->stream));  // packed is freed on return
     return VX_OK;
 }
 

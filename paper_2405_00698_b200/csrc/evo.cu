@@ -143,7 +143,6 @@ struct vx_evo {
     // generation scratch
     DevBuf<int32_t> d_todo, d_dec, perm, iota;
     DevBuf<double> xbuf, sorted, keys_tmp, stats, div;
-    DevBuf<int64_t> hist;
     DevBuf<uint32_t> guard;
     // breeding plan (host parse -> device)
     DevBuf<ChildPlan> d_plan;
@@ -201,9 +200,9 @@ struct vx_evo {
 
 namespace {
 
-// exchange buffer: [fitness P | spring updates P | material histogram cells x NMAT]
+// exchange buffer: [fitness P | spring updates P | packed grids P x diversity_words(cells)]
 size_t xbuf_doubles(const vx_evo* e) {
-    return 2 * static_cast<size_t>(e->P) + static_cast<size_t>(e->cells) * VX_NMAT;
+    return 2 * static_cast<size_t>(e->P) + static_cast<size_t>(e->P) * diversity_words(e->cells);
 }
 
 // The plan's device copy, issued by the plan thread on up_stream: rows and
@@ -289,12 +288,11 @@ vx_status alloc_evo(vx_evo* e) {
     VX_TRY(e->d_dec.alloc(P));
     VX_TRY(e->perm.alloc(P));
     VX_TRY(e->iota.alloc(P));
-    VX_TRY(e->xbuf.alloc(2 * static_cast<size_t>(P) + static_cast<size_t>(e->cells) * VX_NMAT));
+    VX_TRY(e->xbuf.alloc(xbuf_doubles(e)));
     VX_TRY(e->sorted.alloc(P));
     VX_TRY(e->keys_tmp.alloc(P));
     VX_TRY(e->stats.alloc(4));
     VX_TRY(e->div.alloc(1));
-    VX_TRY(e->hist.alloc(static_cast<size_t>(e->cells) * VX_NMAT));
     VX_TRY(e->guard.alloc(1));
     VX_TRY(e->d_plan.alloc(P));
     e->mask_words = (e->np + 31) / 32;
@@ -466,9 +464,9 @@ vx_status evo_begin_body(vx_evo* e, int32_t rank, int32_t world) {
                                  &e->table, &e->cfg.plane, &e->cfg.sim, e->d_todo.p, static_cast<int>(mine.size()),
                                  e->xb(), e->xb() + e->P, nullptr));
     }
-    // this rank's part of the population material histogram (the diversity is
-    // a function of it, population_diversity evolution.hpp:89-105): summed
-    // over ranks with the fitness vector in the exchange buffer
+    // the grids this rank holds, packed into the exchange buffer (zeros for
+    // the others): the all-reduce gathers every grid for the exact
+    // population_diversity (evolution.hpp:89-105) in finish
     {
         std::vector<int32_t> own;
         for (int a = 0; a < e->P; ++a)
@@ -476,8 +474,8 @@ vx_status evo_begin_body(vx_evo* e, int32_t rank, int32_t world) {
         if (!own.empty())
             VX_CUDA(cudaMemcpyAsync(e->d_own.p, own.data(), own.size() * sizeof(int32_t), cudaMemcpyHostToDevice,
                                     ctx->stream));
-        VX_TRY(histogram_sel_dev(ctx, static_cast<int>(own.size()), e->d_own.p, e->cells, e->grid[c].p,
-                                 e->xb() + 2 * e->P));
+        VX_TRY(diversity_pack_dev(ctx, static_cast<int>(own.size()), e->d_own.p, e->cells, e->grid[c].p,
+                                  e->xb() + 2 * e->P));
     }
     // the todo list (all ranks) goes to the device for the merge
     if (!e->todo.empty())
@@ -528,8 +526,8 @@ vx_status vx_evo_finish(vx_evo* e, vx_report* rep) {
     const auto t_fin0 = std::chrono::steady_clock::now();
     VX_TRY(merge_dev(ctx, static_cast<int>(e->todo.size()), e->d_todo.p, e->xb(), e->fit[c].p, e->ev[c].p));
     VX_TRY(sort_stats_dev(ctx, P, e->fit[c].p, e->perm.p, e->sorted.p, e->iota.p, e->keys_tmp.p, e->stats.p));
-    VX_TRY(hist_from_doubles_dev(ctx, e->cells, e->xb() + 2 * P, e->hist.p));  // summed over ranks
-    VX_TRY(diversity_from_hist_dev(ctx, P, e->cells, e->hist.p, e->div.p));
+    // population_diversity over the sorted population (evolution.hpp:265), bit-exact
+    VX_TRY(diversity_exact_dev(ctx, P, e->cells, e->xb() + 2 * P, e->perm.p, e->div.p));
     double st[3], div = 0.0;
     std::vector<double> upd(e->todo.empty() ? 0 : P);
     VX_CUDA(cudaMemcpyAsync(st, e->stats.p, 3 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));

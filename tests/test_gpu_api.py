@@ -139,13 +139,13 @@ def test_sharded_generation_matches_single_process(vx, ctx, world):
     after another), a summed exchange buffer standing in for the NCCL
     all-reduce, then finish() everywhere: reports, populations and RNG streams
     equal the single-process run bit for bit — decode and evaluation sharded,
-    diversity from the summed material histogram."""
+    diversity from the gathered (summed) packed grids."""
     import torch
     cfg = desk(vx, 77, P=12, gens=4)
     single = vx.init_evolution(cfg, ctx)
     ranks = [vx.init_evolution(cfg, ctx) for _ in range(world)]
     n = ranks[0].exchange_buffer()[1]
-    assert n == 2 * 12 + 5 * 27
+    assert n == 2 * 12 + 12 * ((27 + 11) // 12)  # fitness | updates | packed grids (12 cells / double)
     bufs = [torch.zeros(n, dtype=torch.float64, device="cuda") for _ in range(world)]
     for st, b in zip(ranks, bufs):
         st.set_exchange_buffer(b.data_ptr())

@@ -2,12 +2,14 @@
 
 The GPU path shards a generation's children across ranks (vx_evo_begin): a
 rank decodes and evaluates only the individuals it owns, then all-reduces
-(SUM) the (2P + 5 cells)-double exchange buffer [fitness P | work counts P |
-material histogram cells x 5] — zeros for what other ranks own — and breeds
-identically everywhere (vx_evo_finish).  Here the same protocol runs with
-the oracle as the per-rank evaluator: the reduced fitness must equal a
-single-process evaluation bit for bit, the reduced histogram must give the
-reference's population_diversity over all grids (evolution.hpp:89-105), and
+(SUM) the (2P + P W)-double exchange buffer [fitness P | work counts P |
+packed grids P x W, 12 four-bit cells per double] — zeros for what other
+ranks own — and breeds identically everywhere (vx_evo_finish).  Here the
+same protocol runs with the oracle as the per-rank evaluator: the reduced
+fitness must equal a single-process evaluation bit for bit, the reduced
+packed grids must give back every decoded grid exactly (so every rank
+computes the reference's population_diversity, evolution.hpp:89-105, on the
+same grids in the same sorted order), and
 the replicated breeding must give identical populations and RNG states on
 every rank — the GPU analogue of the reference's thread-count invariance
 (test_evolution.cpp:196-215).
@@ -27,14 +29,24 @@ CELLS = GRID ** 3
 SIM = None
 
 
-def diversity_from_histogram(hist, P):
-    """diversity_kernel (csrc/ga.cu): exact integer pair counts per cell."""
-    h = np.asarray(hist, np.int64).reshape(-1, 5)
-    pairs = P * (P - 1) // 2
-    same = (h * (h - (h > 0)) // 2).sum()
-    if P < 2 or len(h) == 0:
-        return 0.0
-    return (float(pairs * len(h) - same) / len(h)) / pairs
+W = (CELLS + 11) // 12  # diversity_words (csrc/diversity.cu)
+
+
+def pack_grid(mat):
+    """pack_kernel (csrc/diversity.cu): 12 four-bit cells per double (< 2^48, exact)."""
+    out = np.zeros(W)
+    for w in range(W):
+        v = 0
+        for k in range(12):
+            c = 12 * w + k
+            if c < len(mat):
+                v |= (int(mat[c]) & 0xF) << (4 * k)
+        out[w] = float(v)
+    return out
+
+
+def unpack_grid(words):
+    return np.array([(int(words[c // 12]) >> (4 * (c % 12))) & 0xF for c in range(CELLS)], np.uint8)
 
 
 def _worker(rank, world, port, out_dir):
@@ -58,21 +70,23 @@ def _worker(rank, world, port, out_dir):
             m, w = lib.decode(8, [12, 12], pop["params"][a], pop["bmat"][a], GRID, GRID, GRID)
             mats.append(m)
             wts.append(w)
-        xbuf = torch.zeros(2 * P + 5 * CELLS, dtype=torch.float64)
+        xbuf = torch.zeros(2 * P + P * W, dtype=torch.float64)
         for a in vx.shard_indices(todo, rank, world):
             xbuf[a] = lib.evaluate_fitness(mats[a], wts[a], GRID, GRID, GRID, sim=sim)
             xbuf[P + a] = 1.0
         for a in vx.shard_indices(list(range(P)), rank, world):  # the grids this rank holds
-            for c in range(CELLS):
-                xbuf[2 * P + 5 * c + int(mats[a][c])] += 1.0
+            xbuf[2 * P + a * W:2 * P + (a + 1) * W] = torch.from_numpy(pack_grid(mats[a]))
         dist.all_reduce(xbuf)
         fit = pop["fitness"].copy()
         for a in todo:
             fit[a] = xbuf[a].item()
         assert xbuf[P:2 * P].sum().item() == len(todo)  # every child evaluated exactly once
-        assert xbuf[2 * P:].sum().item() == P * CELLS     # every grid counted exactly once
-        div = diversity_from_histogram(xbuf[2 * P:].numpy().astype(np.int64), P)
-        np.testing.assert_allclose(div, lib.population_diversity(np.stack(mats)), rtol=1e-13)
+        packed = xbuf[2 * P:].numpy().reshape(P, W)
+        for a in range(P):  # every grid gathered exactly once, bit for bit
+            np.testing.assert_array_equal(unpack_grid(packed[a]), mats[a])
+        order = np.argsort(-fit, kind="stable")  # the sorted population the diversity is taken over
+        div = lib.population_diversity(np.stack([unpack_grid(packed[a]) for a in order]))
+        assert div == lib.population_diversity(np.stack([mats[a] for a in order]))
         ev.set_population(pop["params"], pop["bmat"], fit, np.ones(P, np.uint8), np.stack(mats), np.stack(wts))
         rep = ev.generation()
         np.save(os.path.join(out_dir, f"r{rank}_g{gen}_fit.npy"), fit)
