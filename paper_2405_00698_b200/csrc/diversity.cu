@@ -326,14 +326,13 @@ vx_status diversity_exact_dev(vx_ctx* ctx, int P, int cells, const double* d_pac
     ctx->launches++;
     VX_CUDA(cudaGetLastError());
     // cooperative grid for the ordered sum: one CTA per SM
-    static int coop_ctas = -1;
-    if (coop_ctas < 0) {
+    if (ctx->div_coop_ctas < 0) {
         int per_sm = 0;
         VX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ordered_sum_kernel, kSumThreads, 0));
-        coop_ctas = per_sm > 0 ? ctx->sm_count : 0;
-        if (coop_ctas == 0) return (set_error("diversity: ordered-sum kernel cannot be co-resident"), VX_ECUDA);
+        ctx->div_coop_ctas = per_sm > 0 ? ctx->sm_count : 0;
     }
-    const int G = coop_ctas;
+    if (ctx->div_coop_ctas == 0) return (set_error("diversity: ordered-sum kernel cannot be co-resident"), VX_ECUDA);
+    const int G = ctx->div_coop_ctas;
     VX_TRY(ctx->div_scratch.alloc((sizeof(SumScratch) + G * sizeof(uint64_t) + 7) / 8));
     SumScratch* sc = reinterpret_cast<SumScratch*>(ctx->div_scratch.p);
     VX_CUDA(cudaMemsetAsync(sc, 0, sizeof(double), ctx->stream));  // s = 0
