@@ -439,18 +439,41 @@ vx_status launch_stream_sym(vx_ctx* ctx, vx_batch* b, const StreamArgs& S) {
     A.zero_len2 = S.zero_len2;
     A.zeta2 = S.zeta2;
     A.mu = S.mu;
-    A.L = sym_layout<N>();
-    VX_TRY(ctx->stream_scratch.alloc(A.L.per_robot * static_cast<size_t>(b->n)));
-    A.scratch = ctx->stream_scratch.p;
-    VX_TRY(ctx->stream_ntab.alloc(1));
-    VX_CUDA(cudaMemsetAsync(ctx->stream_ntab.p, 0, sizeof(int32_t), ctx->stream));
-    A.ntab_max = ctx->stream_ntab.p;
-    stream_sym_prep_kernel<N><<<b->n, 1024, 0, ctx->stream>>>(A);
-    ctx->launches++;
-    VX_CUDA(cudaGetLastError());
+    // VX_STREAM_TMA=1: the bulk-copy-fed kernel (when its stage ring + the
+    // batch's actuator tables fit shared memory).  Correct, but 17% slower
+    // than the L1-fed default: the ring couples the warps stage by stage
+    // (profiles/r02_stream_tma.md)
+    const char* tma_env = std::getenv("VX_STREAM_TMA");
+    bool tma = tma_env && *tma_env == '1' && kSymDBuf == 1;
     int32_t ntab = 0;  // shared memory sized for the batch's largest actuator table
-    VX_CUDA(cudaMemcpyAsync(&ntab, ctx->stream_ntab.p, sizeof(int32_t), cudaMemcpyDeviceToHost, ctx->stream));
-    VX_CUDA(cudaStreamSynchronize(ctx->stream));
+    for (int pass = 0; pass < 2; ++pass) {
+        A.L = tma ? sym_layout<N, kTmaT>() : sym_layout<N>();
+        VX_TRY(ctx->stream_scratch.alloc(A.L.per_robot * static_cast<size_t>(b->n)));
+        A.scratch = ctx->stream_scratch.p;
+        VX_TRY(ctx->stream_ntab.alloc(1));
+        VX_CUDA(cudaMemsetAsync(ctx->stream_ntab.p, 0, sizeof(int32_t), ctx->stream));
+        A.ntab_max = ctx->stream_ntab.p;
+        if (tma)
+            stream_sym_prep_kernel<N, kTmaT><<<b->n, 1024, 0, ctx->stream>>>(A);
+        else
+            stream_sym_prep_kernel<N><<<b->n, 1024, 0, ctx->stream>>>(A);
+        ctx->launches++;
+        VX_CUDA(cudaGetLastError());
+        VX_CUDA(cudaMemcpyAsync(&ntab, ctx->stream_ntab.p, sizeof(int32_t), cudaMemcpyDeviceToHost, ctx->stream));
+        VX_CUDA(cudaStreamSynchronize(ctx->stream));
+        if (!tma) break;
+        const size_t smem_t = static_cast<size_t>(kTmaNB) * kStageBytes + 2ull * std::max(1, ntab) * sizeof(double);
+        if (smem_t + 2048 > ctx->smem_optin) {  // tables too large for the ring: the L1-fed kernel
+            tma = false;
+            continue;
+        }
+        VX_CUDA(cudaFuncSetAttribute(stream_sym_tma_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(smem_t)));
+        stream_sym_tma_kernel<N><<<b->n, kTmaThreads, smem_t, ctx->stream>>>(A);
+        ctx->launches++;
+        VX_CUDA(cudaGetLastError());
+        return VX_OK;
+    }
     const size_t smem = (kSymDBuf + 1ull) * std::max(1, ntab) * sizeof(double);
     VX_CUDA(cudaFuncSetAttribute(stream_sym_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(smem)));

@@ -47,7 +47,7 @@ def config4(worlds, steps):
     P = 65536
     cfg = vx.EvolutionConfig(population=P, grid=(10, 10, 10), seed=42, sim=vx.SimConfig(duration=steps * 1e-5))
     st = vx.init_evolution(cfg, ctx)
-    xbuf = torch.zeros(st.exchange_buffer()[1], dtype=torch.float64, device="cuda")  # [fitness|updates|histogram]
+    xbuf = torch.zeros(st.exchange_buffer()[1], dtype=torch.float64, device="cuda")  # [fitness|updates|packed grids]
     st.set_exchange_buffer(xbuf.data_ptr())
     for w in worlds:
         xbuf.zero_()
@@ -56,7 +56,7 @@ def config4(worlds, steps):
         st.begin(0, w)
         ctx.synchronize()
         dt = time.perf_counter() - t0
-        upd = int(xbuf[P:].sum().item())
+        upd = int(xbuf[P:2 * P].sum().item())
         print(json.dumps(dict(config="4 shard", population=P, world=w, rank=0, seconds=dt, spring_updates=upd,
                               updates_per_s=upd / dt, integrator=ctx.last_integrator)), flush=True)
         t1 = time.perf_counter()

@@ -99,3 +99,12 @@ def test_rank_indexed_variants_bit_exact(vx, ctx, orc, dims, kernel, steps):
         np.testing.assert_array_equal(got.robot(r)["pos"], ref.pos, err_msg=f"{dims} robot {r}")
         np.testing.assert_array_equal(got.robot(r)["vel"], ref.vel, err_msg=f"{dims} robot {r}")
         assert out[r].spring_updates == upd
+
+
+@pytest.mark.parametrize("variant", ["free_fast_drive", "soft_slippery", "fine_dt_sticky"])
+def test_stream_tma_kernel_bit_exact(vx, ctx, orc, variant, monkeypatch):
+    """The opt-in bulk-copy-fed 20^3 kernel (VX_STREAM_TMA=1,
+    stream_sym_tma_kernel: warp-specialised producer, mbarrier stage ring)
+    is bit-exact like the default one."""
+    monkeypatch.setenv("VX_STREAM_TMA", "1")
+    test_specialised_integrators_nondefault(vx, ctx, orc, 20, variant)
