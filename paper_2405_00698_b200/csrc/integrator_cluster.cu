@@ -1169,7 +1169,7 @@ vx_status integrate_cluster(vx_ctx* ctx, vx_batch* b, int64_t n_steps, bool writ
         // a filler robot takes ~kFillerRatio cluster-robot times: the filler
         // stops claiming while the clusters still have that much work left
         static const char* ratio_env = std::getenv("VX_FILLER_RATIO");
-        const int ratio = ratio_env ? std::atoi(ratio_env) : 8;
+        const int ratio = ratio_env ? std::atoi(ratio_env) : 6;  // re-swept after the split barriers (profiles/r02_filler.md)
         const int64_t stop_at = static_cast<int64_t>(b->n) - static_cast<int64_t>(slots) * ratio;
         const bool use = slots > 0 && idle > 0 &&
                          ((mode == 1 && stop_at >= idle) || (mode == 2 && b->n > 0));
