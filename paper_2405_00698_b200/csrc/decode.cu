@@ -223,8 +223,12 @@ __global__ void __launch_bounds__(kThreads) decode_kernel(DecodeArgs A) {
 // below kFixGap (orders of magnitude above any DMMA-vs-sequential logit
 // difference) flags its genome, and decode_kernel re-decodes flagged genomes
 // with the exact sequential order (a fix-up launch whose unflagged CTAs exit).
-constexpr int kMmaMT = 4;                    // m-tiles of 8 voxels per tile
-constexpr int kMmaTile = kMmaMT * 8;         // 32 voxels per tile
+#ifndef VX_MMA_MT
+#define VX_MMA_MT 4
+#endif
+constexpr int kMmaMT = VX_MMA_MT;             // m-tiles of 8 voxels per tile
+constexpr int kMmaTile = kMmaMT * 8;         // 32 voxels per tile (default)
+static_assert(kMmaTile <= kThreads && kMmaTile % 32 == 0, "one epilogue thread per voxel of a tile");
 constexpr int kXS = kMmaTile + 4;            // activation row stride (doubles)
 constexpr double kFixGap = 1e-8;             // relative top-2 gap that forces the exact path
 
@@ -330,7 +334,8 @@ __global__ void __launch_bounds__(kThreads) decode_mma_kernel(DecodeArgs A, MmaL
 
     const int ncell = A.w * A.h * A.d;
     const int m = A.m, in0 = 2 * m, in0p = ((in0 + 3) / 4) * 4;
-    bool need_fix = false;
+    __shared__ int s_fix;
+    if (threadIdx.x == 0) s_fix = 0;
     for (int t0 = 0; t0 < ncell; t0 += kMmaTile) {
         // gaussian_encode (genome.hpp:169-179) for 32 voxels; K padding zeroed
         for (int q = threadIdx.x; q < m * kMmaTile; q += kThreads) {
@@ -358,10 +363,10 @@ __global__ void __launch_bounds__(kThreads) decode_mma_kernel(DecodeArgs A, MmaL
         mma_layer<false>(sm + Lo.wf[Lo.nl - 1], sm + Lo.bias[Lo.nl - 1], X, L, Lo.in[Lo.nl - 1], VX_NMAT + 1, wid,
                          lane);
         __syncthreads();
-        if (wid == 0 && t0 + lane < ncell) {
-            const int cell = t0 + lane;
+        if (threadIdx.x < kMmaTile && t0 + static_cast<int>(threadIdx.x) < ncell) {
+            const int vl = threadIdx.x, cell = t0 + vl;
             double lg[VX_NMAT];
-            for (int i = 0; i < VX_NMAT; ++i) lg[i] = L[i * kXS + lane];
+            for (int i = 0; i < VX_NMAT; ++i) lg[i] = L[i * kXS + vl];
             double mx = lg[0];  // std::max_element: first maximal
             for (int i = 1; i < VX_NMAT; ++i)
                 if (mx < lg[i]) mx = lg[i];
@@ -378,18 +383,15 @@ __global__ void __launch_bounds__(kThreads) decode_mma_kernel(DecodeArgs A, MmaL
             double second = -1.0;
             for (int i = 0; i < VX_NMAT; ++i)
                 if (i != best && p[i] > second) second = p[i];
-            if (p[best] - second < kFixGap * p[best]) need_fix = true;
+            if (p[best] - second < kFixGap * p[best]) s_fix = 1;
             const size_t o = static_cast<size_t>(g) * ncell + cell;
-            const double wgt = stable_sigmoid(L[VX_NMAT * kXS + lane]);
+            const double wgt = stable_sigmoid(L[VX_NMAT * kXS + vl]);
             A.mat[o] = static_cast<uint8_t>(best);
             A.weight[o] = wgt < kMinVoxelWeight ? kMinVoxelWeight : (wgt > 1.0 ? 1.0 : wgt);  // morphology.hpp:154
         }
         __syncthreads();
     }
-    if (wid == 0) {
-        need_fix = __any_sync(0xffffffffu, need_fix);
-        if (lane == 0) fix[blockIdx.x] = need_fix ? 1 : 0;
-    }
+    if (threadIdx.x == 0) fix[blockIdx.x] = s_fix ? 1 : 0;  // the tile loop ends with a barrier
 }
 
 // ------------------------------------------------------------ K14: mt19937_64
