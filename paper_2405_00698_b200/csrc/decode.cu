@@ -280,8 +280,9 @@ __device__ __forceinline__ void mma_tile(const double* __restrict__ WF, const do
 
 template <bool kTanh>
 __device__ __forceinline__ void mma_layer(const double* WF, const double* bias, const double* X, double* Y, int in,
-                                          int out, int wid, int lane) {
+                                          int out, int wid, int lane, int rows_x, int rows_y) {
     const int NT = (out + 7) / 8, KS = (in + 3) / 4;
+    VX_DCHECK(KS * 4 <= rows_x && NT * 8 <= rows_y);  // activation rows cover the padded K and N
     if (NT >= kWarps) {
         for (int nt = wid; nt < NT; nt += kWarps) mma_tile<kTanh>(WF, bias, X, Y, KS, nt, 0, kMmaMT, lane);
     } else {
@@ -354,14 +355,14 @@ __global__ void __launch_bounds__(kThreads) decode_mma_kernel(DecodeArgs A, MmaL
             X[(in0 + q / kMmaTile) * kXS + q % kMmaTile] = 0.0;
         __syncthreads();
         for (int l = 0; l + 1 < Lo.nl; ++l) {  // hidden: affine + tanh (genome.hpp:192)
-            mma_layer<true>(sm + Lo.wf[l], sm + Lo.bias[l], X, Y, Lo.in[l], Lo.out[l], wid, lane);
+            mma_layer<true>(sm + Lo.wf[l], sm + Lo.bias[l], X, Y, Lo.in[l], Lo.out[l], wid, lane, Lo.rows, Lo.rows);
             __syncthreads();
             double* t = X;
             X = Y;
             Y = t;
         }
         mma_layer<false>(sm + Lo.wf[Lo.nl - 1], sm + Lo.bias[Lo.nl - 1], X, L, Lo.in[Lo.nl - 1], VX_NMAT + 1, wid,
-                         lane);
+                         lane, Lo.rows, 8);
         __syncthreads();
         if (threadIdx.x < kMmaTile && t0 + static_cast<int>(threadIdx.x) < ncell) {
             const int vl = threadIdx.x, cell = t0 + vl;

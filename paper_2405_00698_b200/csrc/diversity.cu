@@ -94,7 +94,8 @@ __device__ __host__ __forceinline__ int64_t pair_index(int64_t P, int64_t a, int
 // pairs, 256 threads x 2 x 2 pairs in registers; a cell differs when any of
 // its 3 material bit-planes differs: 3 LOP3 + POPC per 32 cells and pair
 __global__ void __launch_bounds__(256) count_kernel(int P, int W32, const uint32_t* __restrict__ planes, int ta0,
-                                                    int ntile, int64_t n_base, uint32_t* __restrict__ cnt) {
+                                                    int ntile, int64_t n_base, int64_t cap,
+                                                    uint32_t* __restrict__ cnt) {
     int64_t rem = blockIdx.x;
     int ta = ta0;
     while (rem >= ntile - ta) {
@@ -130,7 +131,10 @@ __global__ void __launch_bounds__(256) count_kernel(int P, int W32, const uint32
     }
     const int a0 = ta * kTile + ti, b0 = tb * kTile + tj;
     auto put = [&](int a, int b, uint32_t v) {
-        if (a < b && b < P) cnt[pair_index(P, a, b) - n_base] = v;
+        if (a < b && b < P) {
+            VX_DCHECK(pair_index(P, a, b) >= n_base && pair_index(P, a, b) - n_base < cap);
+            cnt[pair_index(P, a, b) - n_base] = v;
+        }
     };
     put(a0, b0, c00);
     put(a0, b0 + 16, c01);
@@ -358,8 +362,9 @@ vx_status diversity_exact_dev(vx_ctx* ctx, int P, int cells, const double* d_pac
         const int64_t a_hi = std::min<int64_t>(P - 1, static_cast<int64_t>(ta1) * kTile);
         const int64_t n_base = pair_index(P, a_lo, a_lo + 1);
         const int64_t n_terms = pair_index(P, a_hi, a_hi + 1) - n_base;
-        count_kernel<<<static_cast<unsigned>(n_tiles_pairs), 256, 0, ctx->stream>>>(P, W32, ctx->div_words.p, ta0,
-                                                                                    ntile, n_base, ctx->div_counts.p);
+        VX_DCHECK_HOST(n_terms <= static_cast<int64_t>(ctx->div_counts.n));
+        count_kernel<<<static_cast<unsigned>(n_tiles_pairs), 256, 0, ctx->stream>>>(
+            P, W32, ctx->div_words.p, ta0, ntile, n_base, static_cast<int64_t>(ctx->div_counts.n), ctx->div_counts.p);
         ctx->launches++;
         VX_CUDA(cudaGetLastError());
         if (n_terms > 0) {

@@ -699,6 +699,7 @@ __device__ void sym_robot_tma(const SymArgs& A, int r, unsigned char* base) {
                 int k1 = (j * T + T + off + 7) & ~7;
                 if (k1 > PCOL) k1 = PCOL;
                 const uint32_t nk = static_cast<uint32_t>(k1 - k0);
+                VX_DCHECK(k0 >= 0 && k1 <= PCOL && nk <= static_cast<uint32_t>(kStageKeys) && nk % 8 == 0);
                 const uint32_t dst = st0 + static_cast<uint32_t>(q) * kStageBytes;
                 const uint32_t fb = full0 + 8u * q;
                 mbar_expect_tx(fb, nk * 18u);
@@ -745,6 +746,7 @@ __device__ void sym_robot_tma(const SymArgs& A, int r, unsigned char* base) {
         const int q = static_cast<int>(s & (kTmaNB - 1));
         mbar_wait(full0 + 8u * q, static_cast<uint32_t>(s / kTmaNB) & 1u);
         const unsigned char* st = stages + q * kStageBytes;
+        VX_DCHECK(li >= 0 && li < kStageKeys);
         kk = reinterpret_cast<const double*>(st)[li];
         r0 = reinterpret_cast<const double*>(st + kStageKeys * 8)[li];
         vox = reinterpret_cast<const uint16_t*>(st + kStageKeys * 16)[li];
