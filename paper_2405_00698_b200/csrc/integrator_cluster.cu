@@ -43,6 +43,10 @@
 #include "vx_cluster.cuh"
 #include "vx_internal.cuh"
 
+#ifndef VX_CL_DRV_EARLY
+#define VX_CL_DRV_EARLY 1  // next step's drive loaded before phase 2 (+1.1%, profiles/r02_split_barrier.md)
+#endif
+
 namespace vx {
 namespace {
 
@@ -725,6 +729,9 @@ __device__ __forceinline__ void cluster_vertex_robot(const ClArgs& A, const int 
 #endif
         int zero_len = 0;
         double sx = 0.0, sy = 0.0, sz = 0.0;
+#if VX_CL_DRV_EARLY == 2
+        const double2 drv_pre = __ldg(A.drive + (kstep + 1 < A.n_steps ? kstep + 1 : kstep));
+#endif
         {
             auto chunk = [&](auto c0_tag, auto n_tag) {
                 constexpr int c0 = decltype(c0_tag)::value, n = decltype(n_tag)::value;
@@ -831,6 +838,10 @@ __device__ __forceinline__ void cluster_vertex_robot(const ClArgs& A, const int 
             break;
         }
 #endif
+#if VX_CL_DRV_EARLY == 1
+        // next step's drive, loaded before phase 2 so the L2 latency overlaps it
+        const double2 drv_next = __ldg(A.drive + (kstep + 1 < A.n_steps ? kstep + 1 : kstep));
+#endif
         int bad = 0;
         double speed_sq = 0.0;
         if (live) {
@@ -914,7 +925,13 @@ __device__ __forceinline__ void cluster_vertex_robot(const ClArgs& A, const int 
             if (speed_sq > max_sq) max_sq = speed_sq;
         }
         if (kstep + 1 < A.n_steps) {
+#if VX_CL_DRV_EARLY == 1
+            const double2 drv = drv_next;
+#elif VX_CL_DRV_EARLY == 2
+            const double2 drv = drv_pre;
+#else
             const double2 drv = __ldg(A.drive + kstep + 1);
+#endif
 #pragma unroll
             for (int j = 0; j < kVpt; ++j) {
                 const int v = a + j * kNmp;
