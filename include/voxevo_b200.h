@@ -271,12 +271,15 @@ vx_status vx_evaluate(vx_ctx* ctx, int32_t P, int32_t w, int32_t h, int32_t d, c
 
 /* ------------------------------------------------- population stats (K11-K12) */
 /* population_diversity (evolution.hpp:89-105) over P grids of `cells`
- * materials, via per-cell material histograms (exact integer pair counts;
- * result within 1e-15 relative of the reference's pairwise sum). */
+ * materials (0..4), in the given order: the reference's double BIT FOR BIT
+ * (pair differ counts, then its ordered running sum of differ/cells
+ * reproduced in parallel, diversity.cu). */
 vx_status vx_population_diversity_dev(vx_ctx* ctx, int32_t P, int32_t cells, const uint8_t* d_mat, double* d_out);
 vx_status vx_population_diversity(vx_ctx* ctx, int32_t P, int32_t cells, const uint8_t* mat, double* out);
-/* Per-cell material counts (cells x 5 int64), the all-reduce operand for
- * sharded diversity, and the diversity value from a (reduced) histogram. */
+/* Per-cell material counts (cells x 5 int64) and the O(P cells) diversity
+ * from a (reduced) histogram: exact pair counts, within 1e-15 relative of the
+ * reference (its rounding sequence is not reproduced; the evolution path uses
+ * the bit-exact form above). */
 vx_status vx_material_histogram_dev(vx_ctx* ctx, int32_t P, int32_t cells, const uint8_t* d_mat,
                                     int64_t* d_hist, int32_t accumulate);
 vx_status vx_diversity_from_histogram_dev(vx_ctx* ctx, int32_t P, int32_t cells, const int64_t* d_hist,

@@ -417,9 +417,9 @@ inline double evaluate_fitness(const VoxelGrid& raw, const MaterialTable& table,
     return evaluate_fitness(std::vector<VoxelGrid>{raw}, table, plane, sim, dev)[0];
 }
 
-// population_diversity (evolution.hpp:89-105) over the raw grids (material
-// histogram per cell on device: exact integer counts, result within 1e-13 of
-// the reference's sequential per-pair sum).
+// population_diversity (evolution.hpp:89-105) over the raw grids: the
+// reference's double bit for bit (pair counts and its ordered running sum,
+// reproduced on device).
 inline double population_diversity(const std::vector<Individual>& pop, Device& dev = default_device()) {
     if (pop.size() < 2) return 0.0;
     const std::size_t cells = pop[0].grid.cells.size();
