@@ -54,3 +54,24 @@ def test_plan_scan_random_sweep(plan_check):
         out = subprocess.run([plan_check, str(P), str(np_), repr(cx), repr(rate), "2", str(skip)],
                              capture_output=True, text=True, timeout=120)
         assert out.returncode == 0, (P, np_, cx, rate, skip, out.stdout)
+
+
+def test_plan_scan_thread_sanitizer(tmp_path):
+    """The scan thread appends mutation chunks while worker threads fill their
+    normals (round-1 advisor: a reallocation race).  ThreadSanitizer over
+    shapes that start the worker pool (many 16k-entry chunks) and a
+    multi-generation run must report no data race, and the results still
+    match the restated loop."""
+    exe = str(tmp_path / "plan_check_tsan")
+    built = subprocess.run(["g++", "-O1", "-g", "-std=c++17", "-pthread", "-fsanitize=thread",
+                            os.path.join(ROOT, "tests", "native", "plan_check.cpp"),
+                            os.path.join(ROOT, "paper_2405_00698_b200", "csrc", "ga_plan.cpp"), "-o", exe],
+                           capture_output=True, text=True)
+    if built.returncode != 0:
+        pytest.skip("ThreadSanitizer unavailable: " + built.stderr[-300:])
+    env = dict(os.environ, TSAN_OPTIONS="halt_on_error=1 exitcode=66")
+    for args in (["2048", "8710", "0.4", "0.1", "2", "0"], ["512", "20000", "0.5", "0.3", "3", "7"]):
+        out = subprocess.run([exe] + args, capture_output=True, text=True, timeout=600, env=env)
+        assert "ThreadSanitizer" not in out.stderr, out.stderr[-3000:]
+        assert out.returncode == 0, out.stdout + out.stderr[-2000:]
+        assert json.loads(out.stdout.strip().splitlines()[-1])["ok"] is True
