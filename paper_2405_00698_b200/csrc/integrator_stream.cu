@@ -477,6 +477,15 @@ vx_status launch_stream_sym(vx_ctx* ctx, vx_batch* b, const StreamArgs& S) {
     const size_t smem = (kSymDBuf + 1ull) * std::max(1, ntab) * sizeof(double);
     VX_CUDA(cudaFuncSetAttribute(stream_sym_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(smem)));
+    {  // the smallest shared-memory carveout that holds the tables: the rest of
+       // the unified L1 serves the neighbour-state reads (default 5.20e10,
+       // minimal carveout 5.30e10, maximal 4.1e10: profiles/README.md)
+        const char* co = std::getenv("VX_STREAM_CARVEOUT");  // A/B: a fixed percentage
+        const int pct = co ? std::atoi(co)
+                           : std::min(100, static_cast<int>((100 * (smem + 4096) + ctx->smem_optin - 1) /
+                                                            ctx->smem_optin) + 2);
+        VX_CUDA(cudaFuncSetAttribute(stream_sym_kernel<N>, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
+    }
     stream_sym_kernel<N><<<b->n, kStreamThreads, smem, ctx->stream>>>(A);
     ctx->launches++;
     VX_CUDA(cudaGetLastError());
