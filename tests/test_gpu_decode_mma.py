@@ -83,3 +83,20 @@ def test_mma_population_bench_shape(vx, ctx, orc):
     np.testing.assert_array_equal(mt, me)
     np.testing.assert_allclose(wt, we, rtol=1e-14, atol=0)
     assert refined <= 8  # gaps < 1e-8 are rare (smallest seen 2.85e-7)
+
+
+def test_wide_network_falls_back_to_exact_kernel(vx, ctx, orc):
+    """Weights too large for shared memory next to the activations (hidden
+    512: ~290 KB): decode runs the exact-order kernel with the genome read
+    from global memory, still bit-exact in materials."""
+    m, hidden, dims = 32, [512], (4, 4, 4)
+    arch = vx.Arch.make(m, hidden)
+    gs = [orc.sample_genome(m, hidden, s) for s in (5, 6, 7)]
+    params = np.stack([g[0] for g in gs])
+    bmat = np.stack([g[1] for g in gs])
+    mt, wt, refined = _decode(vx, params, bmat, arch, dims, ctx, exact=False)
+    assert refined == -1  # the tensor-pipe kernel did not run
+    for a in range(3):
+        rm, rw = orc.decode(m, hidden, params[a], bmat[a], *dims)
+        np.testing.assert_array_equal(mt[a], rm)
+        np.testing.assert_allclose(wt[a], rw, rtol=1e-13)
