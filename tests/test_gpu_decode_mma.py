@@ -86,10 +86,10 @@ def test_mma_population_bench_shape(vx, ctx, orc):
 
 
 def test_wide_network_falls_back_to_exact_kernel(vx, ctx, orc):
-    """Weights too large for shared memory next to the activations (hidden
-    512: ~290 KB): decode runs the exact-order kernel with the genome read
-    from global memory, still bit-exact in materials."""
-    m, hidden, dims = 32, [512], (4, 4, 4)
+    """Weights + activations too large for the tensor-pipe kernel's shared
+    memory (hidden 256: ~300 KB): decode runs the exact-order kernel with the
+    genome read from global memory, still bit-exact in materials."""
+    m, hidden, dims = 32, [256], (4, 4, 4)
     arch = vx.Arch.make(m, hidden)
     gs = [orc.sample_genome(m, hidden, s) for s in (5, 6, 7)]
     params = np.stack([g[0] for g in gs])
