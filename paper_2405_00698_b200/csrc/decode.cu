@@ -63,6 +63,7 @@ struct DecodeArgs {
     double* weight;
     uint32_t* guard;
     bool params_in_smem;
+    int tile;  // voxels per tile (<= 32, one per lane of warp-wide rows; smaller for very wide networks)
     // forward() point queries instead of voxel centres (genome.hpp:187-211):
     // points [genome][n_points][3]; probs [genome][n_points][5] and the
     // unclamped weight head into `weight`
@@ -104,17 +105,19 @@ __global__ void __launch_bounds__(kThreads) decode_kernel(DecodeArgs A) {
     }
     double* Bm = sm;  // 3m
     sm += 3 * A.m;
-    double* X = sm;  // [feature][kTile]
-    double* Y = sm + static_cast<size_t>(A.max_width) * kTile;
-    double* L = Y + static_cast<size_t>(A.max_width) * kTile;  // logits [6][kTile]
+    const int T = A.tile;
+    double* X = sm;  // [feature][T]
+    double* Y = sm + static_cast<size_t>(A.max_width) * T;
+    double* L = Y + static_cast<size_t>(A.max_width) * T;  // logits [6][T]
     for (int q = threadIdx.x; q < 3 * A.m; q += kThreads) Bm[q] = A.bmat[static_cast<size_t>(g) * 3 * A.m + q];
     __syncthreads();
 
     const int ncell = A.points ? A.n_points : A.w * A.h * A.d;
     const int m = A.m;
-    for (int t0 = 0; t0 < ncell; t0 += kTile) {
+    const bool lane_in = lane < T;
+    for (int t0 = 0; t0 < ncell; t0 += T) {
         const int cell = t0 + lane;
-        const bool live = cell < ncell;
+        const bool live = lane_in && cell < ncell;
         double v0 = 0.0, v1 = 0.0, v2 = 0.0;
         if (live && A.points) {
             const double* pt = A.points + (static_cast<size_t>(g) * ncell + cell) * 3;
@@ -132,8 +135,10 @@ __global__ void __launch_bounds__(kThreads) decode_kernel(DecodeArgs A) {
             const double phase = kTwoPi * (Bm[3 * r] * v0 + Bm[3 * r + 1] * v1 + Bm[3 * r + 2] * v2);
             double sn, cs;
             sincos(phase, &sn, &cs);
-            X[r * kTile + lane] = cs;
-            X[(m + r) * kTile + lane] = sn;
+            if (lane_in) {
+                X[r * T + lane] = cs;
+                X[(m + r) * T + lane] = sn;
+            }
         }
         __syncthreads();
         // hidden layers: affine (genome.hpp:118-126) + tanh (:192)
@@ -146,8 +151,9 @@ __global__ void __launch_bounds__(kThreads) decode_kernel(DecodeArgs A) {
             for (int r = wid; r < out; r += kWarps) {
                 const double* wr = W + static_cast<int64_t>(r) * in;
                 double acc = b[r];
-                for (int c = 0; c < in; ++c) acc += wr[c] * X[c * kTile + lane];
-                Y[r * kTile + lane] = tanh(acc);
+                if (!lane_in) continue;
+                for (int c = 0; c < in; ++c) acc += wr[c] * X[c * T + lane];
+                Y[r * T + lane] = tanh(acc);
             }
             __syncthreads();
             double* t = X;
@@ -165,14 +171,15 @@ __global__ void __launch_bounds__(kThreads) decode_kernel(DecodeArgs A) {
             for (int r = wid; r < VX_NMAT + 1; r += kWarps) {
                 const double* wr = r < VX_NMAT ? Wm + static_cast<int64_t>(r) * in : Ww;
                 double acc = r < VX_NMAT ? bm[r] : bw[0];
-                for (int c = 0; c < in; ++c) acc += wr[c] * X[c * kTile + lane];
-                L[r * kTile + lane] = acc;
+                if (!lane_in) continue;
+                for (int c = 0; c < in; ++c) acc += wr[c] * X[c * T + lane];
+                L[r * T + lane] = acc;
             }
         }
         __syncthreads();
         if (wid == 0 && live) {
             double lg[VX_NMAT];
-            for (int i = 0; i < VX_NMAT; ++i) lg[i] = L[i * kTile + lane];
+            for (int i = 0; i < VX_NMAT; ++i) lg[i] = L[i * T + lane];
             double mx = lg[0];  // std::max_element: first maximal
             for (int i = 1; i < VX_NMAT; ++i)
                 if (mx < lg[i]) mx = lg[i];
@@ -184,7 +191,7 @@ __global__ void __launch_bounds__(kThreads) decode_kernel(DecodeArgs A) {
             }
             for (int i = 0; i < VX_NMAT; ++i) p[i] /= sum;
             const size_t o = static_cast<size_t>(g) * ncell + cell;
-            const double wgt = stable_sigmoid(L[VX_NMAT * kTile + lane]);
+            const double wgt = stable_sigmoid(L[VX_NMAT * T + lane]);
             if (A.probs) {  // forward(): MaterialQuery{probs, weight}
                 for (int i = 0; i < VX_NMAT; ++i) A.probs[o * VX_NMAT + i] = p[i];
                 A.weight[o] = wgt;
@@ -581,11 +588,21 @@ vx_status forward_dev(vx_ctx* ctx, const vx_arch* a, int P, const double* d_para
     return launch_decode(ctx, a, np, maxw, A, P);
 }
 
+// activation buffers of the exact kernel for a tile of `tile` voxels
+static size_t exact_act_bytes(int maxw, int m, int tile) {
+    return (2ull * maxw + VX_NMAT + 1) * tile * sizeof(double) + 3ull * m * sizeof(double);
+}
+// the widest voxel tile (32, 16, .., 1) whose activations fit shared memory; 0 if none
+static int exact_tile(const vx_ctx* ctx, int maxw, int m) {
+    for (int t = kTile; t >= 1; t /= 2)
+        if (exact_act_bytes(maxw, m, t) + 1024 <= ctx->smem_optin) return t;
+    return 0;
+}
+
 vx_status decode_feasible(vx_ctx* ctx, const vx_arch* a) {
     int maxw = 2 * a->m;
     for (int l = 0; l < a->n_hidden; ++l) maxw = maxw > a->hidden[l] ? maxw : a->hidden[l];
-    const size_t act = (2ull * maxw + VX_NMAT + 1) * kTile * sizeof(double) + 3ull * a->m * sizeof(double);
-    if (act > ctx->smem_optin) return (set_error("decode: architecture too wide"), VX_EINVAL);
+    if (exact_tile(ctx, maxw, a->m) == 0) return (set_error("decode: architecture too wide"), VX_EINVAL);
     return VX_OK;
 }
 
@@ -622,11 +639,15 @@ static bool mma_layout(const vx_ctx* ctx, const vx_arch* a, MmaLayout& Lo, size_
 }
 
 vx_status launch_decode(vx_ctx* ctx, const vx_arch* a, int64_t np, int maxw, DecodeArgs& A, int n) {
-    const size_t act = (2ull * maxw + VX_NMAT + 1) * kTile * sizeof(double) + 3ull * a->m * sizeof(double);
+    // exact kernel: 32-voxel tiles with the genome in shared memory when it
+    // fits, else the genome read from global memory, else narrower tiles
+    // (very wide networks: the reference accepts any width)
+    A.tile = exact_tile(ctx, maxw, a->m);
+    if (A.tile == 0) return (set_error("decode: architecture too wide"), VX_EINVAL);
+    const size_t act = exact_act_bytes(maxw, a->m, A.tile);
     size_t smem = act + static_cast<size_t>(np) * sizeof(double);
-    A.params_in_smem = smem + 1024 <= ctx->smem_optin;
+    A.params_in_smem = A.tile == kTile && smem + 1024 <= ctx->smem_optin;
     if (!A.params_in_smem) smem = act;
-    if (smem > ctx->smem_optin) return (set_error("decode: architecture too wide"), VX_EINVAL);
     // decode(): the MLP layers on the FP64 tensor pipe, exact re-decode of flagged
     // genomes; forward() point queries and VX_DECODE=exact keep the CUDA-core kernel
     std::pair<cudaEvent_t, cudaEvent_t> ev{nullptr, nullptr};

@@ -85,11 +85,14 @@ def test_mma_population_bench_shape(vx, ctx, orc):
     assert refined <= 8  # gaps < 1e-8 are rare (smallest seen 2.85e-7)
 
 
-def test_wide_network_falls_back_to_exact_kernel(vx, ctx, orc):
+@pytest.mark.parametrize("hidden", [[256], [512], [2048], [600, 40]])
+def test_wide_network_falls_back_to_exact_kernel(vx, ctx, orc, hidden):
     """Weights + activations too large for the tensor-pipe kernel's shared
     memory (hidden 256: ~300 KB): decode runs the exact-order kernel with the
-    genome read from global memory, still bit-exact in materials."""
-    m, hidden, dims = 32, [256], (4, 4, 4)
+    genome read from global memory — and for very wide layers (512, 2048)
+    on narrower voxel tiles — still bit-exact in materials (the reference
+    accepts any width)."""
+    m, dims = 32, (4, 4, 4)
     arch = vx.Arch.make(m, hidden)
     gs = [orc.sample_genome(m, hidden, s) for s in (5, 6, 7)]
     params = np.stack([g[0] for g in gs])
