@@ -656,13 +656,28 @@ __device__ __forceinline__ void cluster_vertex_robot(const ClArgs& A, const int 
     X[5 * XS + PAD + a] = v2;
     const unsigned wmask = __reduce_or_sync(0xffffffffu, bmask);
     double com_start[3] = {0.0, 0.0, 0.0};
+    // center_of_mass sums (rank 0): the CTA stages (mass, x, y, z) in mass
+    // order into the free part of the force-slot area with coalesced loads,
+    // then one thread adds them in the reference's order from shared memory
+    // instead of walking four global arrays serially
+    double* CS = F + (NV + 1) / 2 + 8 + 2 * NTV;  // past the MAP / phase staging of the prologue
+    static_assert((NV + 1) / 2 + 8 + 2 * NTV + 4 * NV <= 39 * kNmp, "COM staging fits the force slots");
+    if (out) {  // CTA-uniform (rank 0)
+        for (int q = a; q < nm; q += kNmp) {
+            CS[q] = b.mass[mo + q];
+            CS[NV + q] = b.pos[mo + q];
+            CS[2 * NV + q] = b.pos[b.M + mo + q];
+            CS[3 * NV + q] = b.pos[2 * b.M + mo + q];
+        }
+        __syncthreads();
+    }
     if (out && a == 0) {  // center_of_mass (physics.hpp:266-278) of the initial state, in mass order
         double c0 = 0.0, c1 = 0.0, c2 = 0.0, total = 0.0;
         for (int q = 0; q < nm; ++q) {
-            const double w = b.mass[mo + q];
-            c0 += w * b.pos[mo + q];
-            c1 += w * b.pos[b.M + mo + q];
-            c2 += w * b.pos[2 * b.M + mo + q];
+            const double w = CS[q];
+            c0 += w * CS[NV + q];
+            c1 += w * CS[2 * NV + q];
+            c2 += w * CS[3 * NV + q];
             total += w;
         }
         if (total > 0.0) {
@@ -987,16 +1002,25 @@ __device__ __forceinline__ void cluster_vertex_robot(const ClArgs& A, const int 
     }
     __threadfence();
     cluster_barrier();
+    if (out) {  // stage the final positions for the COM (no remote store reaches F any more)
+        for (int q = a; q < nm; q += kNmp) {
+            CS[q] = b.mass[mo + q];
+            CS[NV + q] = A.xfinal[mo + q];
+            CS[2 * NV + q] = A.xfinal[b.M + mo + q];
+            CS[3 * NV + q] = A.xfinal[2 * b.M + mo + q];
+        }
+        __syncthreads();
+    }
     if (out && a == 0) {
         double mx = 0.0;
         for (int c = 0; c < CL; ++c)
             if (s_cmax[c] > mx) mx = s_cmax[c];
         double c0 = 0.0, c1 = 0.0, c2 = 0.0, total = 0.0;
         for (int q = 0; q < nm; ++q) {
-            const double w = b.mass[mo + q];
-            c0 += w * A.xfinal[mo + q];
-            c1 += w * A.xfinal[b.M + mo + q];
-            c2 += w * A.xfinal[2 * b.M + mo + q];
+            const double w = CS[q];
+            c0 += w * CS[NV + q];
+            c1 += w * CS[2 * NV + q];
+            c2 += w * CS[3 * NV + q];
             total += w;
         }
         if (total > 0.0) {
