@@ -103,3 +103,20 @@ def test_wide_network_falls_back_to_exact_kernel(vx, ctx, orc, hidden):
         rm, rw = orc.decode(m, hidden, params[a], bmat[a], *dims)
         np.testing.assert_array_equal(mt[a], rm)
         np.testing.assert_allclose(wt[a], rw, rtol=1e-13)
+
+
+def test_decode_timing_and_dmma_peak(vx, ctx):
+    """The bench line's decode roofline inputs: live CUDA-event time and voxel
+    count of decode launches (vx_decode_timing) and the measured DMMA peak."""
+    arch = vx.Arch.make()
+    params, bmat = vx.sample_genomes(arch, [3, 4, 5, 6], ctx)
+    ctx.timing(True)
+    ctx.decode_time(reset=True)
+    vx.decode(params, bmat, arch, 5, 5, 5, ctx)
+    vx.decode(params[:2], bmat[:2], arch, 4, 4, 4, ctx)
+    ms, voxels = ctx.decode_time(reset=True)
+    ctx.timing(False)
+    assert ms > 0.0 and voxels == 4 * 125 + 2 * 64
+    assert ctx.decode_time(reset=True) == (0.0, 0)
+    peak = ctx.dmma_peak_tflops()
+    assert 10.0 < peak < 100.0, peak  # B200: ~37 TFLOP/s FP64 on DMMA
